@@ -1,0 +1,355 @@
+// extern "C" boundary (include/symdist_b200.h). Every entry point catches and maps
+// exceptions to sdb_status; the message is kept per thread for sdb_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "../../include/symdist_b200.h"
+#include "engine.hpp"
+#include "errors.hpp"
+#include "gf2.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+sdb_status guarded(F &&f) {
+    try {
+        f();
+        g_last_error.clear();
+        return SDB_OK;
+    } catch (const sdb::ParseFailure &e) {
+        g_last_error = e.what();
+        return SDB_ERR_PARSE;
+    } catch (const sdb::ValidationFailure &e) {
+        g_last_error = e.what();
+        return SDB_ERR_VALIDATION;
+    } catch (const sdb::InternalFailure &e) {
+        g_last_error = e.what();
+        return SDB_ERR_INTERNAL;
+    } catch (const sdb::DeviceFailure &e) {
+        g_last_error = e.what();
+        return SDB_ERR_DEVICE;
+    } catch (const std::invalid_argument &e) {
+        g_last_error = e.what();
+        return SDB_ERR_INVALID_ARGUMENT;
+    } catch (const std::bad_alloc &) {
+        g_last_error = "host allocation failed";
+        return SDB_ERR_INTERNAL;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return SDB_ERR_INTERNAL;
+    }
+}
+
+void check_matrix_args(const uint64_t *rows, int n_rows, int n_cols, int row_words) {
+    if (n_rows < 0 || n_cols < 0) throw sdb::InvalidArgument("negative matrix shape");
+    if (n_rows > 0 && !rows) throw sdb::InvalidArgument("null matrix pointer");
+    if (row_words < (n_cols + 63) / 64) throw sdb::InvalidArgument("row_words smaller than ceil(n_cols/64)");
+}
+
+sdb_run_options opts_or_default(const sdb_run_options *o) {
+    sdb_run_options d;
+    sdb_default_options(&d);
+    return o ? *o : d;
+}
+
+void zero_report(sdb_report *r) {
+    std::memset(r, 0, sizeof *r);
+    r->best_generation = -1;
+    r->best_gamma = -1;
+}
+
+// saved_isometry (distance.cpp:135-149): validate -> isometry -> information_sets ->
+// filter from the original rows -> run_bz -> U/2
+void saved_isometry_impl(const uint64_t *rows, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
+                         sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_matrix_args(rows, n_rows, n_cols, row_words);
+    if (n_cols == 0 || n_cols % 2 != 0)
+        throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+    zero_report(rep);
+    const sdb::BitMat a = sdb::BitMat::from_words(rows, n_rows, n_cols, row_words);
+    const int n = n_cols / 2, k = n_rows - n;
+    if (o.validate) {
+        const sdb::Validation v = sdb::validate_normalizer(a);
+        if (!v.ok) throw sdb::ValidationFailure(v.message);
+    }
+    std::vector<sdb::InfoSet> is = sdb::information_sets(sdb::isometry_transform(a));
+    std::vector<sdb::GammaIn> gammas;
+    for (sdb::InfoSet &s : is) gammas.push_back(sdb::GammaIn{std::move(s.matrix), s.rank_deficit});
+    sdb::Filter f;
+    f.enabled = o.dual_filter && k >= 1;
+    if (f.enabled) f.rows = a;
+    const auto tp = std::chrono::steady_clock::now();
+    sdb::Plan plan(std::move(gammas), sdb::Mode::hamming, n, f, o);
+    plan.run(rep, trace, trace_cap, best_out, nullptr);
+    rep->prep_seconds = std::chrono::duration<double>(tp - t0).count() + plan.h2d_seconds;
+    if (rep->complete && rep->upper % 2 != 0)
+        throw sdb::InternalFailure("saved_isometry: image Hamming distance must be even");
+    rep->distance = int(rep->upper / 2);
+    rep->algorithm = SDB_ALG_SAVED_ISOMETRY;
+    rep->workers = o.workers;
+    rep->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+struct sdb_plan {
+    sdb::Plan *plan;
+    int n;
+    int algorithm;
+    sdb_run_options opts;
+    double prep_seconds;
+};
+
+extern "C" {
+
+void sdb_default_options(sdb_run_options *o) {
+    std::memset(o, 0, sizeof *o);
+    o->workers = 1;
+    o->validate = 1;
+    o->dual_filter = 1;
+    o->device = 0;
+    o->max_generation = 0;
+    o->rank = 0;
+    o->world = 1;
+}
+
+const char *sdb_last_error(void) { return g_last_error.c_str(); }
+
+int sdb_abi_version(void) { return SDB_ABI_VERSION; }
+
+int sdb_device_available(void) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        g_last_error = e != cudaSuccess ? cudaGetErrorString(e) : "no CUDA device";
+        cudaGetLastError();
+        return 0;
+    }
+    return 1;
+}
+
+sdb_status sdb_saved_isometry(const uint64_t *rows, int n_rows, int n_cols, int row_words, const sdb_run_options *opts,
+                              sdb_report *report, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out) {
+    return guarded([&] {
+        if (!report) throw sdb::InvalidArgument("null report");
+        saved_isometry_impl(rows, n_rows, n_cols, row_words, opts_or_default(opts), report, trace, trace_cap,
+                            best_out);
+    });
+}
+
+sdb_status sdb_compute_distance(const uint64_t *rows, int n_rows, int n_cols, int row_words, int algorithm,
+                                const sdb_run_options *opts, sdb_report *report, sdb_trace_entry *trace,
+                                int trace_cap) {
+    return guarded([&] {
+        if (!report) throw sdb::InvalidArgument("null report");
+        const int k = n_rows - n_cols / 2;
+        switch (algorithm) {
+            case SDB_ALG_SAVED_ISOMETRY:
+                break;
+            case SDB_ALG_AUTO:
+                // distance.cpp:233-237: auto sends k <= 2 to saved_2_gamma
+                if (k <= 2) throw sdb::InvalidArgument("compute_distance: auto selects saved_2_gamma for k <= 2, "
+                                                       "which this build does not provide yet");
+                break;
+            case SDB_ALG_SAVED_1_GAMMA:
+            case SDB_ALG_SAVED_2_GAMMA:
+            case SDB_ALG_BRUTE_FORCE:
+                throw sdb::InvalidArgument("compute_distance: algorithm not provided by this build yet");
+            default:
+                throw sdb::InvalidArgument("compute_distance: unknown algorithm");
+        }
+        saved_isometry_impl(rows, n_rows, n_cols, row_words, opts_or_default(opts), report, trace, trace_cap,
+                            nullptr);
+    });
+}
+
+sdb_status sdb_saved_isometry_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words,
+                                    const sdb_run_options *opts, int *distances, int *statuses, int *generations,
+                                    sdb_trace_entry *traces, int *trace_lens, int trace_cap, double *elapsed_seconds,
+                                    double *device_seconds) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (n_codes < 0) throw sdb::InvalidArgument("negative code count");
+        check_matrix_args(rows, n_rows * std::max(n_codes, 0), n_cols, row_words);
+        if (!distances || !statuses || !generations || !trace_lens || (trace_cap > 0 && !traces))
+            throw sdb::InvalidArgument("null output array");
+        sdb::run_batch(rows, n_codes, n_rows, n_cols, row_words, opts_or_default(opts), distances, statuses,
+                       generations, traces, trace_lens, trace_cap, device_seconds);
+        if (elapsed_seconds)
+            *elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+sdb_status sdb_run_bz(const uint64_t *gammas, int n_gammas, int n_rows, int n_cols, int row_words, int mode,
+                      int pair_count, const int *rank_deficits, const uint64_t *filter_rows, int filter_n_rows,
+                      int filter_n_cols, int filter_row_words, int filter_enabled, int filter_k,
+                      const sdb_run_options *opts, sdb_report *report, sdb_trace_entry *trace, int trace_cap,
+                      uint64_t *best_out) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!report) throw sdb::InvalidArgument("null report");
+        if (n_gammas <= 0) throw sdb::InvalidArgument("run_bz: need at least one generator matrix");
+        check_matrix_args(gammas, n_rows * n_gammas, n_cols, row_words);
+        if (mode != SDB_MODE_SYMPLECTIC && mode != SDB_MODE_HAMMING) throw sdb::InvalidArgument("unknown weight mode");
+        zero_report(report);
+        std::vector<sdb::GammaIn> gs;
+        for (int j = 0; j < n_gammas; j++)
+            gs.push_back(sdb::GammaIn{sdb::BitMat::from_words(gammas + size_t(j) * n_rows * row_words, n_rows, n_cols,
+                                                              row_words),
+                                      rank_deficits ? rank_deficits[j] : 0});
+        sdb::Filter f;
+        f.enabled = filter_enabled && filter_k >= 1;
+        if (f.enabled) {
+            check_matrix_args(filter_rows, filter_n_rows, filter_n_cols, filter_row_words);
+            f.rows = sdb::BitMat::from_words(filter_rows, filter_n_rows, filter_n_cols, filter_row_words);
+        }
+        const sdb_run_options o = opts_or_default(opts);
+        sdb::Plan plan(std::move(gs), mode == SDB_MODE_HAMMING ? sdb::Mode::hamming : sdb::Mode::symplectic,
+                       pair_count, f, o);
+        plan.run(report, trace, trace_cap, best_out, nullptr);
+        report->distance = int(report->upper);
+        report->workers = o.workers;
+        report->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+sdb_status sdb_lower_bound(int g, int mode, int n_gammas, const int *rank_deficits, const int *n_packages,
+                           const int *n_pp, long long *out) {
+    return guarded([&] {
+        if (n_gammas <= 0) throw sdb::InvalidArgument("lower_bound: no generator matrices");
+        if (!out) throw sdb::InvalidArgument("null output");
+        if (mode == SDB_MODE_HAMMING) {
+            long long s = 0;
+            for (int j = 0; j < n_gammas; j++) s += std::max(0LL, (long long)g + 1 - (rank_deficits ? rank_deficits[j] : 0));
+            *out = s;
+            return;
+        }
+        if (n_gammas == 1) {
+            *out = (long long)g + 1;
+            return;
+        }
+        if (n_gammas == 2) {
+            const long long np = n_packages ? n_packages[1] : 0, npp = n_pp ? n_pp[1] : 0;
+            *out = (long long)g + 1 + std::max(0LL, (long long)g + 1 + npp - np);
+            return;
+        }
+        throw sdb::InvalidArgument("lower_bound: symplectic mode takes one or two matrices");
+    });
+}
+
+sdb_status sdb_validate_normalizer(const uint64_t *rows, int n_rows, int n_cols, int row_words, int *ok, char *msg,
+                                   int msg_len) {
+    return guarded([&] {
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        if (n_cols == 0 || n_cols % 2 != 0)
+            throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+        const sdb::Validation v = sdb::validate_normalizer(sdb::BitMat::from_words(rows, n_rows, n_cols, row_words));
+        if (ok) *ok = v.ok ? 1 : 0;
+        if (msg && msg_len > 0) {
+            std::strncpy(msg, v.message.c_str(), size_t(msg_len) - 1);
+            msg[msg_len - 1] = 0;
+        }
+    });
+}
+
+sdb_status sdb_isometry_transform(const uint64_t *rows, int n_rows, int n_cols, int row_words, uint64_t *out,
+                                  int out_row_words) {
+    return guarded([&] {
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        const sdb::BitMat img = sdb::isometry_transform(sdb::BitMat::from_words(rows, n_rows, n_cols, row_words));
+        if (out_row_words < img.stride) throw sdb::InvalidArgument("out_row_words too small");
+        img.to_words(out, out_row_words);
+    });
+}
+
+sdb_status sdb_information_sets(const uint64_t *rows, int n_rows, int n_cols, int row_words, int max_gammas,
+                                uint64_t *out, int out_row_words, int *deficits, int *pivots, int *n_gammas) {
+    return guarded([&] {
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        if (out_row_words < (n_cols + 63) / 64) throw sdb::InvalidArgument("out_row_words too small");
+        const std::vector<sdb::InfoSet> is =
+            sdb::information_sets(sdb::BitMat::from_words(rows, n_rows, n_cols, row_words));
+        if (n_gammas) *n_gammas = int(is.size());
+        for (int j = 0; j < int(is.size()) && j < max_gammas; j++) {
+            is[size_t(j)].matrix.to_words(out + size_t(j) * n_rows * out_row_words, out_row_words);
+            if (deficits) deficits[j] = is[size_t(j)].rank_deficit;
+            if (pivots)
+                for (int i = 0; i < n_rows; i++) pivots[size_t(j) * n_rows + i] = is[size_t(j)].pivots[size_t(i)];
+        }
+    });
+}
+
+sdb_status sdb_generate_code(int n, int k, uint64_t seed, int transvections, uint64_t *out, int out_row_words) {
+    return guarded([&] {
+        if (!out) throw sdb::InvalidArgument("null output");
+        const sdb::BitMat a = sdb::generate_code(n, k, seed, transvections);
+        if (out_row_words < a.stride) throw sdb::InvalidArgument("out_row_words too small");
+        a.to_words(out, out_row_words);
+    });
+}
+
+sdb_status sdb_plan_create(const uint64_t *rows, int n_rows, int n_cols, int row_words, const sdb_run_options *opts,
+                           sdb_plan **out) {
+    return guarded([&] {
+        if (!out) throw sdb::InvalidArgument("null plan output");
+        *out = nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        if (n_cols == 0 || n_cols % 2 != 0)
+            throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+        const sdb_run_options o = opts_or_default(opts);
+        const sdb::BitMat a = sdb::BitMat::from_words(rows, n_rows, n_cols, row_words);
+        const int n = n_cols / 2, k = n_rows - n;
+        if (o.validate) {
+            const sdb::Validation v = sdb::validate_normalizer(a);
+            if (!v.ok) throw sdb::ValidationFailure(v.message);
+        }
+        std::vector<sdb::InfoSet> is = sdb::information_sets(sdb::isometry_transform(a));
+        std::vector<sdb::GammaIn> gammas;
+        for (sdb::InfoSet &s : is) gammas.push_back(sdb::GammaIn{std::move(s.matrix), s.rank_deficit});
+        sdb::Filter f;
+        f.enabled = o.dual_filter && k >= 1;
+        if (f.enabled) f.rows = a;
+        auto *p = new sdb_plan{nullptr, n, SDB_ALG_SAVED_ISOMETRY, o, 0};
+        try {
+            p->plan = new sdb::Plan(std::move(gammas), sdb::Mode::hamming, n, f, o);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        p->prep_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = p;
+    });
+}
+
+sdb_status sdb_plan_run(sdb_plan *plan, sdb_report *report, sdb_trace_entry *trace, int trace_cap,
+                        double *level_seconds) {
+    return guarded([&] {
+        if (!plan || !report) throw sdb::InvalidArgument("null plan or report");
+        const auto t0 = std::chrono::steady_clock::now();
+        zero_report(report);
+        plan->plan->run(report, trace, trace_cap, nullptr, level_seconds);
+        if (report->complete && report->upper % 2 != 0)
+            throw sdb::InternalFailure("saved_isometry: image Hamming distance must be even");
+        report->distance = int(report->upper / 2);
+        report->algorithm = plan->algorithm;
+        report->workers = plan->opts.workers;
+        report->prep_seconds = plan->prep_seconds;
+        report->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+void sdb_plan_destroy(sdb_plan *plan) {
+    if (!plan) return;
+    delete plan->plan;
+    delete plan;
+}
+
+}  // extern "C"

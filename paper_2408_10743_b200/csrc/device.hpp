@@ -1,0 +1,75 @@
+// Shared host/device description of one enumeration problem (all Gamma_j of one code,
+// singleton packages) and the kernel entry points in kernels.cu.
+//
+// HBM layout (one allocation per plan, all 16-byte aligned):
+//   rows  u32 [G][N][2W]   row r of Gamma_j: W x-words then W z-words (bit i of the
+//                          x-block = column i of the first half, i.e. the reference's
+//                          EnumMatrix symplectic split, engine.cpp:58-97)
+//   syn   u64 [G][N][SW]   compressed admissibility syndrome of each row (SW=0: no filter)
+//   binom u64 [N+1][BK]    saturating binomials C(a,b), b < BK
+//   state LevelState       per-level running minimum + per-weight best keys
+// Weight of a candidate = scale * sum_i popc(x_i | z_i); scale = 2 on the isometry
+// route (Hamming weight of (a|b|a^b) = 2 popc(a|b), prep.hpp:66-68), 1 otherwise.
+#pragma once
+
+#include <cstdint>
+
+namespace sdb {
+
+constexpr int kMaxW = 8;         // u32 words per half: n <= 256
+constexpr int kMaxSW = 4;        // u64 syndrome words: 2k <= 256
+constexpr int kMaxG = 64;        // matrices per code
+constexpr int kMaxLevel = 62;    // combination size handled by the kernels
+constexpr int kKeyRankBits = 58; // key = gamma << 58 | lexicographic rank
+constexpr uint64_t kNoKey = ~uint64_t(0);
+
+struct LevelState {
+    unsigned int wmin;           // min weight found this level (engine units), ~0u: none
+    unsigned int pad;
+    unsigned long long visited;  // candidates the kernels enumerated
+    // followed in memory by key_by_w[max_weight + 1] (u64)
+};
+
+struct ProblemDev {
+    const uint32_t *rows;
+    const unsigned long long *syn;
+    const unsigned long long *binom;
+    LevelState *state;
+    unsigned long long *key_by_w;
+    int G, N, W, SW, BK;
+    int scale;
+    int max_weight;
+};
+
+struct LevelLaunch {
+    int g;
+    unsigned int thr0;            // only candidates with weight <= thr0 are considered (U - 1)
+    unsigned long long per_gamma; // C(N, g)
+    unsigned long long seg_len;   // lexicographic ranks per walk segment
+    unsigned long long segs_per_gamma;
+    unsigned long long seg_begin, seg_end;  // this rank's shard of [0, G * segs_per_gamma)
+};
+
+// One level, all matrices, lexicographic-walk kernel. Returns the number of kernels launched.
+int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, int num_sms);
+
+// One level, all matrices, head x tail tile kernel (large levels).
+struct TilePlan;
+int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms);
+
+// Batch: one code per CTA, the whole level loop on the device.
+struct BatchDev {
+    const uint32_t *rows;      // [codes][G][N][2W]
+    const unsigned long long *syn;       // [codes][G][N][SW]
+    const int *deficits;       // [codes][G]
+    const unsigned long long *binom;     // [N+1][BK]
+    int *out_upper;            // [codes] final U (engine units)
+    int *out_generations;      // [codes]
+    int *out_status;           // [codes] 0 ok, 3 no admissible codeword
+    int *out_trace_lower;      // [codes][N]
+    int *out_trace_upper;      // [codes][N]
+    int codes, G, N, W, SW, BK, scale, sentinel;
+};
+int launch_batch(const BatchDev &b, void *stream);
+
+}  // namespace sdb

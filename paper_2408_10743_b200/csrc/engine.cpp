@@ -1,0 +1,485 @@
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <thread>
+
+#include "errors.hpp"
+
+namespace sdb {
+
+size_t problem_smem_bytes(int G, int N, int W, int SW, int BK);
+
+void check_cuda(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw DeviceFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+std::vector<unsigned long long> binom_table(int N, int BK) {
+    const unsigned long long cap = 1ull << 62;
+    std::vector<unsigned long long> t(size_t(N + 1) * BK, 0);
+    for (int a = 0; a <= N; a++)
+        for (int b = 0; b < BK && b <= a; b++) {
+            if (b == 0 || b == a) {
+                t[size_t(a) * BK + b] = 1;
+            } else {
+                const unsigned long long x = t[size_t(a - 1) * BK + b - 1], y = t[size_t(a - 1) * BK + b];
+                t[size_t(a) * BK + b] = (x >= cap || y >= cap || x + y >= cap) ? cap : x + y;
+            }
+        }
+    return t;
+}
+
+static unsigned long long binom_u64(int a, int b) {
+    if (b < 0 || a < 0 || b > a) return 0;
+    if (b > a - b) b = a - b;
+    unsigned __int128 r = 1;
+    for (int i = 1; i <= b; i++) {
+        r = r * unsigned(a - b + i) / unsigned(i);
+        if (r >> 62) return 1ull << 62;
+    }
+    return (unsigned long long)r;
+}
+
+// bits of row r at columns [from, from+len) packed into u32 words
+static void extract_bits(const BitMat &m, int r, int from, int len, uint32_t *dst, int words) {
+    for (int i = 0; i < words; i++) dst[i] = 0;
+    for (int c = 0; c < len; c++)
+        if (m.get(r, from + c)) dst[c >> 5] |= 1u << (c & 31);
+}
+
+int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, std::vector<uint64_t> &out) {
+    out.clear();
+    if (!f.enabled) return 0;
+    const int G = int(gammas.size()), N = gammas[0].matrix.rows, F = f.rows.rows;
+    // S: (G*N) x F, bit (i, r) = <first 2n columns of Gamma row i, filter row r>_s
+    BitMat S(G * N, F);
+    std::vector<uint64_t> proj(size_t((2 * n + 63) / 64));
+    for (int j = 0; j < G; j++)
+        for (int i = 0; i < N; i++) {
+            std::fill(proj.begin(), proj.end(), 0);
+            for (int c = 0; c < 2 * n; c++)
+                if (gammas[size_t(j)].matrix.get(i, c)) proj[size_t(c >> 6)] |= uint64_t(1) << (c & 63);
+            for (int r = 0; r < F; r++)
+                if (symplectic_ip(proj.data(), f.rows.row(r), n)) S.set(j * N + i, r, true);
+        }
+    // every candidate syndrome lies in rowspace(S); it is zero iff it vanishes on the
+    // pivot columns of S's echelon form, so keep only those columns
+    BitMat E = S;
+    const std::vector<int> piv = echelonize(E);
+    const int rk = int(piv.size());
+    const int SW = std::max(1, (rk + 63) / 64);
+    if (SW > kMaxSW) throw InvalidArgument("admissibility syndrome wider than 256 bits (k > 128)");
+    out.assign(size_t(G) * N * SW, 0);
+    for (int i = 0; i < G * N; i++)
+        for (int b = 0; b < rk; b++)
+            if (S.get(i, piv[size_t(b)])) out[size_t(i) * SW + (b >> 6)] |= uint64_t(1) << (b & 63);
+    return SW;
+}
+
+Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter &filter, const sdb_run_options &opts)
+    : gammas_(std::move(gammas)), mode_(mode), pair_count_(pair_count), opts_(opts) {
+    if (gammas_.empty()) throw InvalidArgument("run_bz: need at least one generator matrix");
+    G_ = int(gammas_.size());
+    if (G_ > kMaxG) throw InvalidArgument("run_bz: too many generator matrices");
+    N_ = gammas_[0].matrix.rows;
+    const int cols = gammas_[0].matrix.cols;
+    for (const GammaIn &g : gammas_)
+        if (g.matrix.cols != cols || g.matrix.rows != N_)
+            throw InvalidArgument("run_bz: generator matrices must share one codeword frame");
+    if (N_ == 0) throw InvalidArgument("run_bz: matrix with no packages");
+    const int n = pair_count_;
+    if (filter.enabled && filter.rows.cols != 2 * n)
+        throw InvalidArgument("enumerate_generation: filter frame mismatch");
+
+    // weight layout
+    std::vector<uint32_t> xw, zw;
+    if (mode_ == Mode::symplectic) {
+        if (cols != 2 * n) throw InvalidArgument("symplectic mode needs 2n columns");
+        W_ = (n + 31) / 32;
+        scale_ = 1;
+        max_weight_ = n;
+        sentinel_ = n + 1;
+        image_layout_ = true;
+    } else {
+        sentinel_ = cols + 1;
+        max_weight_ = cols;
+        bool image = n > 0 && cols == 3 * n;
+        for (int j = 0; image && j < G_; j++)
+            for (int r = 0; image && r < N_; r++)
+                for (int i = 0; i < n; i++) {
+                    const BitMat &m = gammas_[size_t(j)].matrix;
+                    if (m.get(r, 2 * n + i) != (m.get(r, i) != m.get(r, n + i))) { image = false; break; }
+                }
+        image_layout_ = image;
+        if (image) {
+            W_ = (n + 31) / 32;
+            scale_ = 2;
+        } else {
+            W_ = (cols + 31) / 32;
+            scale_ = 1;
+        }
+    }
+    if (W_ < 1) W_ = 1;
+    if (W_ > kMaxW) throw InvalidArgument("rows too wide for the enumeration kernels (n > 256)");
+    h_rows_.assign(size_t(G_) * N_ * 2 * W_, 0);
+    for (int j = 0; j < G_; j++)
+        for (int r = 0; r < N_; r++) {
+            uint32_t *dst = h_rows_.data() + (size_t(j) * N_ + r) * 2 * W_;
+            const BitMat &m = gammas_[size_t(j)].matrix;
+            if (image_layout_) {
+                extract_bits(m, r, 0, n, dst, W_);
+                extract_bits(m, r, n, n, dst + W_, W_);
+            } else {
+                extract_bits(m, r, 0, cols, dst, W_);
+            }
+        }
+    SW_ = build_syndromes(gammas_, n, filter, h_syn_);
+    BK_ = std::min(N_, kMaxLevel) + 2;
+    h_binom_ = binom_table(N_, BK_);
+    upload();
+}
+
+Plan::~Plan() {
+    if (d_mem_) cudaFree(d_mem_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+void Plan::upload() {
+    device_ = opts_.device;
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    check_cuda(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_), "cudaDeviceGetAttribute");
+    check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    check_cuda(cudaEventCreate(&ev0_), "cudaEventCreate");
+    check_cuda(cudaEventCreate(&ev1_), "cudaEventCreate");
+    const size_t b_rows = align256(h_rows_.size() * 4), b_syn = align256(std::max<size_t>(h_syn_.size(), 1) * 8),
+                 b_binom = align256(h_binom_.size() * 8),
+                 b_state = align256(sizeof(LevelState) + size_t(max_weight_ + 1) * 8);
+    const auto t0 = std::chrono::steady_clock::now();
+    check_cuda(cudaMalloc(&d_mem_, b_rows + b_syn + b_binom + b_state), "cudaMalloc");
+    unsigned char *base = static_cast<unsigned char *>(d_mem_);
+    check_cuda(cudaMemcpyAsync(base, h_rows_.data(), h_rows_.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D rows");
+    if (!h_syn_.empty())
+        check_cuda(cudaMemcpyAsync(base + b_rows, h_syn_.data(), h_syn_.size() * 8, cudaMemcpyHostToDevice, stream_),
+                   "H2D syn");
+    check_cuda(cudaMemcpyAsync(base + b_rows + b_syn, h_binom_.data(), h_binom_.size() * 8, cudaMemcpyHostToDevice,
+                               stream_),
+               "H2D binom");
+    check_cuda(cudaStreamSynchronize(stream_), "H2D sync");
+    h2d_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    pd_.rows = reinterpret_cast<const uint32_t *>(base);
+    pd_.syn = reinterpret_cast<const unsigned long long *>(base + b_rows);
+    pd_.binom = reinterpret_cast<const unsigned long long *>(base + b_rows + b_syn);
+    pd_.state = reinterpret_cast<LevelState *>(base + b_rows + b_syn + b_binom);
+    pd_.key_by_w = reinterpret_cast<unsigned long long *>(base + b_rows + b_syn + b_binom + sizeof(LevelState));
+    pd_.G = G_;
+    pd_.N = N_;
+    pd_.W = W_;
+    pd_.SW = SW_;
+    pd_.BK = BK_;
+    pd_.scale = scale_;
+    pd_.max_weight = max_weight_;
+    h_state_.assign(sizeof(LevelState) + size_t(max_weight_ + 1) * 8, 0);
+    if (problem_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
+        throw InvalidArgument("problem too large for shared-memory staging");
+}
+
+long long Plan::lower_bound(int g) const {
+    // engine.cpp:31-47 for singleton packages: hamming sums over matrices; symplectic
+    // single matrix g+1; two matrices g+1+max(0, g+1+n_pp-n_p) with n_pp = n_p here.
+    if (mode_ == Mode::hamming) {
+        long long s = 0;
+        for (const GammaIn &gm : gammas_) s += std::max(0LL, (long long)g + 1 - gm.rank_deficit);
+        return s;
+    }
+    if (G_ == 1) return (long long)g + 1;
+    if (G_ == 2) return (long long)g + 1 + std::max(0LL, (long long)g + 1);
+    throw InvalidArgument("lower_bound: symplectic mode takes one or two matrices");
+}
+
+void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out, double *level_seconds) {
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    const int world = std::max(1, opts_.world), rank = opts_.rank;
+    if (rank < 0 || rank >= world) throw InvalidArgument("rank outside [0, world)");
+    if (world > 1 && !opts_.allreduce_min) throw InvalidArgument("world > 1 needs an allreduce_min callback");
+    long long U = sentinel_, L = 1;
+    int generation = 0, launches = 0;
+    unsigned long long candidates = 0, visited = 0;
+    double enum_s = 0;
+    int best_g = -1, best_j = -1;
+    unsigned long long best_r = 0;
+    int g_limit = N_;
+    if (opts_.max_generation > 0) g_limit = std::min(g_limit, opts_.max_generation);
+    bool complete = false;
+    int n_levels = 0;
+    const int threads_total = num_sms_ * 8 * 256;
+    for (int g = 1; g <= g_limit; g++) {
+        if (g > kMaxLevel) throw InvalidArgument("generation beyond the kernels' combination-size limit");
+        const unsigned long long per = binom_u64(N_, g);
+        if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
+        LevelLaunch LL{};
+        LL.g = g;
+        LL.thr0 = unsigned(U - 1);
+        LL.per_gamma = per;
+        const unsigned long long total = per * (unsigned long long)G_;
+        unsigned long long seg = (total + (unsigned long long)threads_total * 4 - 1) / ((unsigned long long)threads_total * 4);
+        LL.seg_len = std::max<unsigned long long>(64, seg);
+        LL.segs_per_gamma = (per + LL.seg_len - 1) / LL.seg_len;
+        const unsigned long long S = LL.segs_per_gamma * (unsigned long long)G_;
+        LL.seg_begin = (unsigned long long)((unsigned __int128)S * rank / world);
+        LL.seg_end = (unsigned long long)((unsigned __int128)S * (rank + 1) / world);
+        check_cuda(cudaMemsetAsync(pd_.state, 0xFF, h_state_.size(), stream_), "memset state");
+        check_cuda(cudaMemsetAsync(&pd_.state->visited, 0, 8, stream_), "memset visited");
+        check_cuda(cudaEventRecord(ev0_, stream_), "event");
+        const int nl = launch_walk_level(pd_, LL, stream_, num_sms_);
+        if (nl < 0) throw InvalidArgument("unsupported row width");
+        launches += nl;
+        check_cuda(cudaGetLastError(), "walk kernel launch");
+        check_cuda(cudaEventRecord(ev1_, stream_), "event");
+        check_cuda(cudaMemcpyAsync(h_state_.data(), pd_.state, h_state_.size(), cudaMemcpyDeviceToHost, stream_),
+                   "D2H state");
+        check_cuda(cudaStreamSynchronize(stream_), "level sync");
+        float ms = 0;
+        check_cuda(cudaEventElapsedTime(&ms, ev0_, ev1_), "event time");
+        enum_s += ms * 1e-3;
+        LevelState st;
+        std::memcpy(&st, h_state_.data(), sizeof st);
+        const unsigned long long *keys = reinterpret_cast<const unsigned long long *>(h_state_.data() + sizeof st);
+        uint64_t wmin = st.wmin == ~0u ? ~uint64_t(0) : uint64_t(st.wmin);
+        uint64_t key = wmin != ~uint64_t(0) ? keys[wmin] : kNoKey;
+        visited += st.visited;
+        if (world > 1) {
+            uint64_t v = wmin;
+            if (opts_.allreduce_min(opts_.allreduce_ctx, &v, 1) != 0) throw DeviceFailure("allreduce_min failed");
+            if (v != wmin) key = kNoKey;
+            wmin = v;
+            uint64_t k2 = key;
+            if (opts_.allreduce_min(opts_.allreduce_ctx, &k2, 1) != 0) throw DeviceFailure("allreduce_min failed");
+            key = k2;
+        }
+        if (wmin != ~uint64_t(0) && (long long)wmin < U) {
+            U = (long long)wmin;
+            best_g = g;
+            best_j = int(key >> kKeyRankBits);
+            best_r = key & ((1ull << kKeyRankBits) - 1);
+        }
+        candidates += total;
+        generation = g;
+        L = lower_bound(g);
+        if (n_levels < trace_cap && trace) trace[n_levels] = sdb_trace_entry{g, L, U};
+        if (level_seconds && n_levels < trace_cap) level_seconds[n_levels] = ms * 1e-3;
+        n_levels++;
+        if (L >= U) { complete = true; break; }
+        if (g == N_) complete = true;
+    }
+    if (complete && U >= sentinel_)
+        throw InternalFailure("run_bz: no admissible codeword after complete enumeration; "
+                              "input is not a valid normalizer matrix");
+    rep->generations = generation;
+    rep->candidates_enumerated = candidates;
+    rep->trace_len = n_levels;
+    rep->complete = complete ? 1 : 0;
+    rep->upper = U;
+    rep->candidates_visited = visited;
+    rep->enum_seconds = enum_s;
+    rep->n_gammas = G_;
+    rep->kernel_launches = launches;
+    rep->best_generation = best_g;
+    rep->best_gamma = best_j;
+    rep->best_rank = best_r;
+    if (best_out) {
+        const BitMat &m = gammas_[size_t(std::max(0, best_j))].matrix;
+        std::vector<uint64_t> acc(size_t(m.stride), 0);
+        if (best_g > 0) {
+            // lexicographic unrank (host twin of the kernels' unrank_lex)
+            unsigned long long r = best_r;
+            int v = 0;
+            for (int i = 0; i < best_g; i++) {
+                for (;; v++) {
+                    const unsigned long long cnt = binom_u64(N_ - 1 - v, best_g - 1 - i);
+                    if (r < cnt) break;
+                    r -= cnt;
+                }
+                for (int w = 0; w < m.stride; w++) acc[size_t(w)] ^= m.row(v)[w];
+                v++;
+            }
+        }
+        std::copy(acc.begin(), acc.end(), best_out);
+    }
+}
+
+// ------------------------------------------------------------------------------- batch
+
+void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
+               int *distances, int *statuses, int *generations, sdb_trace_entry *traces, int *trace_lens,
+               int trace_cap, double *device_seconds) {
+    if (n_codes <= 0) return;
+    if (n_cols % 2 != 0 || n_cols == 0)
+        throw InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+    const int n = n_cols / 2, k = n_rows - n, N = n_rows;
+    const int W = (n + 31) / 32;
+    if (W > kMaxW) throw InvalidArgument("rows too wide for the enumeration kernels (n > 256)");
+    struct Prepped {
+        int status = 0;
+        std::vector<GammaIn> gammas;
+        std::vector<uint64_t> syn;
+        int SW = 0;
+    };
+    std::vector<Prepped> pp(static_cast<size_t>(n_codes));
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nthreads = int(std::min<unsigned>(hw, unsigned(n_codes)));
+    auto work = [&](int t) {
+        for (int c = t; c < n_codes; c += nthreads) {
+            Prepped &p = pp[size_t(c)];
+            try {
+                BitMat a = BitMat::from_words(rows + size_t(c) * n_rows * row_words, n_rows, n_cols, row_words);
+                if (o.validate) {
+                    Validation v = validate_normalizer(a);
+                    if (!v.ok) { p.status = SDB_ERR_VALIDATION; continue; }
+                }
+                std::vector<InfoSet> is = information_sets(isometry_transform(a));
+                for (InfoSet &s : is) p.gammas.push_back(GammaIn{std::move(s.matrix), s.rank_deficit});
+                Filter f;
+                f.enabled = o.dual_filter && k >= 1;
+                if (f.enabled) f.rows = a;
+                p.SW = build_syndromes(p.gammas, n, f, p.syn);
+            } catch (const ValidationFailure &) {
+                p.status = SDB_ERR_VALIDATION;
+            } catch (const std::exception &) {
+                p.status = SDB_ERR_INTERNAL;
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nthreads; t++) pool.emplace_back(work, t);
+    work(0);
+    for (std::thread &t : pool) t.join();
+
+    int G = 0, SW = 0;
+    std::vector<int> live;
+    for (int c = 0; c < n_codes; c++)
+        if (pp[size_t(c)].status == 0) {
+            live.push_back(c);
+            G = std::max(G, int(pp[size_t(c)].gammas.size()));
+            SW = std::max(SW, pp[size_t(c)].SW);
+        }
+    for (int c = 0; c < n_codes; c++) {
+        statuses[c] = pp[size_t(c)].status;
+        distances[c] = -1;
+        generations[c] = 0;
+        trace_lens[c] = 0;
+    }
+    if (device_seconds) *device_seconds = 0;
+    if (live.empty()) return;
+    const int nl = int(live.size());
+    const int BK = std::min(N, kMaxLevel) + 2;
+    std::vector<uint32_t> h_rows(size_t(nl) * G * N * 2 * W, 0);
+    std::vector<uint64_t> h_syn(size_t(nl) * G * N * SW, 0);
+    std::vector<int> h_def(size_t(nl) * G, 1 << 20);
+    for (int li = 0; li < nl; li++) {
+        const Prepped &p = pp[size_t(live[size_t(li)])];
+        for (int j = 0; j < G; j++) {
+            // codes with fewer matrices repeat their first one with a deficit that never
+            // contributes to L (duplicates cannot lower the minimum)
+            const int src = j < int(p.gammas.size()) ? j : 0;
+            const BitMat &m = p.gammas[size_t(src)].matrix;
+            if (j < int(p.gammas.size())) h_def[size_t(li) * G + j] = p.gammas[size_t(j)].rank_deficit;
+            for (int r = 0; r < N; r++) {
+                uint32_t *dst = h_rows.data() + ((size_t(li) * G + j) * N + r) * 2 * W;
+                extract_bits(m, r, 0, n, dst, W);
+                extract_bits(m, r, n, n, dst + W, W);
+                for (int s = 0; s < p.SW; s++)
+                    h_syn[((size_t(li) * G + j) * N + r) * SW + s] = p.syn[(size_t(src) * N + r) * p.SW + s];
+            }
+        }
+    }
+    std::vector<unsigned long long> h_binom = binom_table(N, BK);
+    check_cuda(cudaSetDevice(o.device), "cudaSetDevice");
+    cudaStream_t st;
+    check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    const size_t b_rows = align256(h_rows.size() * 4), b_syn = align256(std::max<size_t>(h_syn.size(), 1) * 8),
+                 b_def = align256(h_def.size() * 4), b_binom = align256(h_binom.size() * 8),
+                 b_out = align256(size_t(nl) * 4);
+    const size_t b_tr = align256(size_t(nl) * N * 4);
+    void *mem = nullptr;
+    check_cuda(cudaMalloc(&mem, b_rows + b_syn + b_def + b_binom + 3 * b_out + 2 * b_tr), "cudaMalloc");
+    unsigned char *base = static_cast<unsigned char *>(mem);
+    BatchDev bd{};
+    bd.rows = reinterpret_cast<const uint32_t *>(base);
+    bd.syn = reinterpret_cast<const unsigned long long *>(base + b_rows);
+    bd.deficits = reinterpret_cast<const int *>(base + b_rows + b_syn);
+    bd.binom = reinterpret_cast<const unsigned long long *>(base + b_rows + b_syn + b_def);
+    unsigned char *outp = base + b_rows + b_syn + b_def + b_binom;
+    bd.out_upper = reinterpret_cast<int *>(outp);
+    bd.out_generations = reinterpret_cast<int *>(outp + b_out);
+    bd.out_status = reinterpret_cast<int *>(outp + 2 * b_out);
+    bd.out_trace_lower = reinterpret_cast<int *>(outp + 3 * b_out);
+    bd.out_trace_upper = reinterpret_cast<int *>(outp + 3 * b_out + b_tr);
+    bd.codes = nl;
+    bd.G = G;
+    bd.N = N;
+    bd.W = W;
+    bd.SW = SW;
+    bd.BK = BK;
+    bd.scale = 2;
+    bd.sentinel = 3 * n + 1;
+    try {
+        check_cuda(cudaMemcpyAsync(base, h_rows.data(), h_rows.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+        if (!h_syn.empty())
+            check_cuda(cudaMemcpyAsync(base + b_rows, h_syn.data(), h_syn.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+        check_cuda(cudaMemcpyAsync(base + b_rows + b_syn, h_def.data(), h_def.size() * 4, cudaMemcpyHostToDevice, st),
+                   "H2D");
+        check_cuda(cudaMemcpyAsync(base + b_rows + b_syn + b_def, h_binom.data(), h_binom.size() * 8,
+                                   cudaMemcpyHostToDevice, st),
+                   "H2D");
+        if (problem_smem_bytes(G, N, W, SW, BK) > 200 * 1024) throw InvalidArgument("batch codes too large");
+        cudaEvent_t e0, e1;
+        check_cuda(cudaEventCreate(&e0), "event");
+        check_cuda(cudaEventCreate(&e1), "event");
+        check_cuda(cudaEventRecord(e0, st), "event");
+        if (launch_batch(bd, st) < 0) throw InvalidArgument("unsupported row width");
+        check_cuda(cudaGetLastError(), "batch kernel launch");
+        check_cuda(cudaEventRecord(e1, st), "event");
+        const size_t nls = static_cast<size_t>(nl);
+        std::vector<int> up(nls), gen(nls), stt(nls), tl(nls * N), tu(nls * N);
+        check_cuda(cudaMemcpyAsync(up.data(), bd.out_upper, size_t(nl) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(gen.data(), bd.out_generations, size_t(nl) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(stt.data(), bd.out_status, size_t(nl) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(tl.data(), bd.out_trace_lower, size_t(nl) * N * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(tu.data(), bd.out_trace_upper, size_t(nl) * N * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaStreamSynchronize(st), "batch sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (device_seconds) *device_seconds = ms * 1e-3;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        for (int li = 0; li < nl; li++) {
+            const int c = live[size_t(li)];
+            generations[c] = gen[size_t(li)];
+            trace_lens[c] = gen[size_t(li)];
+            for (int g = 0; g < gen[size_t(li)] && g < trace_cap; g++)
+                traces[size_t(c) * trace_cap + g] =
+                    sdb_trace_entry{g + 1, tl[size_t(li) * N + g], tu[size_t(li) * N + g]};
+            if (stt[size_t(li)] != 0) {
+                statuses[c] = SDB_ERR_INTERNAL;
+            } else if (up[size_t(li)] % 2 != 0) {
+                statuses[c] = SDB_ERR_INTERNAL;
+            } else {
+                distances[c] = up[size_t(li)] / 2;
+            }
+        }
+    } catch (...) {
+        cudaFree(mem);
+        cudaStreamDestroy(st);
+        throw;
+    }
+    cudaFree(mem);
+    cudaStreamDestroy(st);
+}
+
+}  // namespace sdb

@@ -1,0 +1,91 @@
+// Host engine: builds device problems from Gamma_j, runs the level loop
+// (reference run_bz, engine.cpp:303-343) with one kernel launch per level, and the
+// batch path (one code per CTA).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "device.hpp"
+#include "gf2.hpp"
+#include "../../include/symdist_b200.h"
+
+namespace sdb {
+
+enum class Mode { symplectic = 0, hamming = 1 };
+
+// One prepared matrix (singleton packages, prep.hpp:25-35 with packages[i] = {pivot, {i}}).
+struct GammaIn {
+    BitMat matrix;
+    int rank_deficit = 0;
+};
+
+struct Filter {
+    bool enabled = false;
+    BitMat rows;  // rows spanning C_perp in the frame of the first 2n columns
+};
+
+struct LevelResult {
+    int g = 0;
+    long long lower = 0, upper = 0;
+    double seconds = 0;
+    bool improved = false;
+    int best_gamma = -1;
+    unsigned long long best_rank = 0;
+};
+
+class Plan {
+   public:
+    Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter &filter, const sdb_run_options &opts);
+    ~Plan();
+    Plan(const Plan &) = delete;
+    Plan &operator=(const Plan &) = delete;
+
+    // Runs the generation loop from device-resident data; fills report/trace (trace_cap
+    // entries) and, when best_out != nullptr, the best codeword in the Gamma frame.
+    void run(sdb_report *report, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out,
+             double *level_seconds);
+
+    double h2d_seconds = 0;
+    int n_gammas() const { return G_; }
+    int sentinel() const { return sentinel_; }
+
+   private:
+    void upload();
+    long long lower_bound(int g) const;
+    int pick_W_and_pack();
+
+    std::vector<GammaIn> gammas_;
+    Mode mode_;
+    int pair_count_;
+    sdb_run_options opts_;
+    int G_ = 0, N_ = 0, W_ = 0, SW_ = 0, BK_ = 0, scale_ = 1, max_weight_ = 0, sentinel_ = 0;
+    bool image_layout_ = false;
+    std::vector<uint32_t> h_rows_;
+    std::vector<uint64_t> h_syn_;
+    std::vector<unsigned long long> h_binom_;
+    int device_ = 0, num_sms_ = 148;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    void *d_mem_ = nullptr;
+    ProblemDev pd_{};
+    std::vector<unsigned char> h_state_;
+};
+
+// Saturating binomial table (N+1) x BK.
+std::vector<unsigned long long> binom_table(int N, int BK);
+
+// Compressed syndromes for all rows of all gammas (G*N rows), filter semantics of
+// AdmissibilityFilter::for_rows; returns SW (0 when disabled).
+int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, std::vector<uint64_t> &out);
+
+void check_cuda(cudaError_t e, const char *what);
+
+// Batch of same-shape normalizers, one code per CTA.
+void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
+               int *distances, int *statuses, int *generations, sdb_trace_entry *traces, int *trace_lens,
+               int trace_cap, double *device_seconds);
+
+}  // namespace sdb

@@ -1,0 +1,205 @@
+#include "gf2.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "errors.hpp"
+
+namespace sdb {
+
+BitMat BitMat::from_words(const uint64_t *src, int rows, int cols, int row_words) {
+    BitMat m(rows, cols);
+    const int copy = std::min(row_words, m.stride);
+    for (int r = 0; r < rows; r++) {
+        for (int i = 0; i < copy; i++) m.row(r)[i] = src[size_t(r) * row_words + i];
+        if (cols & 63) m.row(r)[m.stride - 1] &= (~uint64_t(0)) >> (64 - (cols & 63));
+    }
+    return m;
+}
+
+void BitMat::to_words(uint64_t *dst, int row_words) const {
+    for (int r = 0; r < rows; r++)
+        for (int i = 0; i < row_words; i++) dst[size_t(r) * row_words + i] = i < stride ? row(r)[i] : 0;
+}
+
+std::string BitMat::row_string(int r) const {
+    std::string s(size_t(cols), '0');
+    for (int c = 0; c < cols; c++)
+        if (get(r, c)) s[size_t(c)] = '1';
+    return s;
+}
+
+std::vector<int> echelonize(BitMat &m) {
+    std::vector<int> pivots;
+    int r = 0;
+    for (int c = 0; c < m.cols && r < m.rows; c++) {
+        const int wi = c >> 6;
+        const uint64_t bit = uint64_t(1) << (c & 63);
+        int sel = -1;
+        for (int i = r; i < m.rows; i++)
+            if (m.row(i)[wi] & bit) { sel = i; break; }
+        if (sel < 0) continue;
+        m.swap_rows(r, sel);
+        for (int i = 0; i < m.rows; i++)
+            if (i != r && (m.row(i)[wi] & bit)) m.xor_into(i, r);
+        pivots.push_back(c);
+        r++;
+    }
+    return pivots;
+}
+
+int rank(const BitMat &m) {
+    BitMat c = m;
+    return int(echelonize(c).size());
+}
+
+BitMat null_space(const BitMat &m) {
+    BitMat ech = m;
+    const std::vector<int> pivots = echelonize(ech);
+    std::vector<char> is_pivot(size_t(m.cols), 0);
+    for (int c : pivots) is_pivot[size_t(c)] = 1;
+    BitMat basis(m.cols - int(pivots.size()), m.cols);
+    int out = 0;
+    for (int f = 0; f < m.cols; f++) {
+        if (is_pivot[size_t(f)]) continue;
+        basis.set(out, f, true);
+        for (size_t r = 0; r < pivots.size(); r++)
+            if (ech.get(int(r), f)) basis.set(out, pivots[r], true);
+        out++;
+    }
+    return basis;
+}
+
+static BitMat swap_halves(const BitMat &a) {
+    const int n = a.cols / 2;
+    BitMat s(a.rows, a.cols);
+    for (int r = 0; r < a.rows; r++)
+        for (int i = 0; i < n; i++) {
+            if (a.get(r, n + i)) s.set(r, i, true);
+            if (a.get(r, i)) s.set(r, n + i, true);
+        }
+    return s;
+}
+
+Validation validate_normalizer(const BitMat &a) {
+    const int rows = a.rows;
+    const int n = a.cols / 2;
+    const int k = rows - n;
+    if (rows == 0) return {false, "matrix has no rows"};
+    if (k < 0) return {false, "matrix has fewer rows than n; a normalizer needs n+k >= n rows"};
+    if (rows > 2 * n) return {false, "matrix has more rows than columns; rows cannot be independent"};
+    if (rank(a) != rows) return {false, "rows are linearly dependent (rank below n+k)"};
+    const BitMat dual = null_space(swap_halves(a));
+    BitMat ech = a;
+    const std::vector<int> pivots = echelonize(ech);
+    std::vector<uint64_t> res(size_t(a.stride));
+    for (int r = 0; r < dual.rows; r++) {
+        std::copy(dual.row(r), dual.row(r) + dual.stride, res.begin());
+        for (size_t p = 0; p < pivots.size(); p++)
+            if ((res[size_t(pivots[p] >> 6)] >> (pivots[p] & 63)) & 1u)
+                for (int i = 0; i < a.stride; i++) res[size_t(i)] ^= ech.row(int(p))[i];
+        bool zero = true;
+        for (uint64_t x : res) zero = zero && x == 0;
+        if (!zero)
+            return {false, "not a stabilizer normalizer: dual vector " + dual.row_string(r) +
+                               " lies outside the rowspace"};
+    }
+    return {true, ""};
+}
+
+BitMat isometry_transform(const BitMat &a) {
+    if (a.cols % 2 != 0) throw InvalidArgument("isometry_transform: column count must be even");
+    const int n = a.cols / 2;
+    BitMat out(a.rows, 3 * n);
+    for (int r = 0; r < a.rows; r++)
+        for (int i = 0; i < n; i++) {
+            const bool ai = a.get(r, i), bi = a.get(r, n + i);
+            if (ai) out.set(r, i, true);
+            if (bi) out.set(r, n + i, true);
+            if (ai != bi) out.set(r, 2 * n + i, true);
+        }
+    return out;
+}
+
+std::vector<InfoSet> information_sets(const BitMat &b) {
+    const int n_rows = b.rows, n_cols = b.cols;
+    if (rank(b) != n_rows) throw ValidationFailure("information_sets: rows are linearly dependent");
+    std::vector<char> used(size_t(n_cols), 0);
+    std::vector<InfoSet> out;
+    BitMat cur = b;
+    for (;;) {
+        std::vector<int> pivot_cols;
+        int r = 0;
+        for (int c = 0; c < n_cols && r < n_rows; c++) {
+            if (used[size_t(c)]) continue;
+            const int wi = c >> 6;
+            const uint64_t bit = uint64_t(1) << (c & 63);
+            int sel = -1;
+            for (int i = r; i < n_rows; i++)
+                if (cur.row(i)[wi] & bit) { sel = i; break; }
+            if (sel < 0) continue;
+            cur.swap_rows(r, sel);
+            for (int i = 0; i < n_rows; i++)
+                if (i != r && (cur.row(i)[wi] & bit)) cur.xor_into(i, r);
+            pivot_cols.push_back(c);
+            r++;
+        }
+        if (pivot_cols.empty()) break;
+        InfoSet is;
+        is.matrix = cur;
+        is.rank_deficit = n_rows - int(pivot_cols.size());
+        is.pivots.assign(size_t(n_rows), -1);
+        for (size_t i = 0; i < pivot_cols.size(); i++) is.pivots[i] = pivot_cols[i];
+        for (int c : pivot_cols) used[size_t(c)] = 1;
+        out.push_back(std::move(is));
+    }
+    return out;
+}
+
+static uint64_t xorshift64star(uint64_t &s) {
+    s ^= s >> 12;
+    s ^= s << 25;
+    s ^= s >> 27;
+    return s * 0x2545F4914F6CDD1DULL;
+}
+
+int symplectic_ip(const uint64_t *u, const uint64_t *v, int n) {
+    // bits [0,n) are x, [n,2n) are z
+    int par = 0;
+    for (int i = 0; i < n; i++) {
+        const int xi = int((u[i >> 6] >> (i & 63)) & 1u), zi = int((u[(n + i) >> 6] >> ((n + i) & 63)) & 1u);
+        const int vx = int((v[i >> 6] >> (i & 63)) & 1u), vz = int((v[(n + i) >> 6] >> ((n + i) & 63)) & 1u);
+        par ^= (xi & vz) ^ (zi & vx);
+    }
+    return par;
+}
+
+BitMat generate_code(int n, int k, uint64_t seed, int transvections) {
+    if (n <= 0 || k < 0 || k > n) throw InvalidArgument("generate_code: need 0 <= k <= n, n >= 1");
+    if (seed == 0) throw InvalidArgument("generate_code: xorshift64* needs a nonzero seed");
+    if (transvections <= 0) transvections = 4 * n;
+    const int rows = n + k, cols = 2 * n;
+    BitMat a(rows, cols);
+    int r = 0;
+    for (int i = 0; i < n - k; i++) a.set(r++, n + i, true);
+    for (int i = n - k; i < n; i++) a.set(r++, i, true);
+    for (int i = n - k; i < n; i++) a.set(r++, n + i, true);
+    BitMat v(1, cols);
+    uint64_t s = seed;
+    const int words = (cols + 63) / 64;
+    for (int t = 0; t < transvections; t++) {
+        for (;;) {
+            for (int w = 0; w < words; w++) v.row(0)[w] = xorshift64star(s);
+            if (cols & 63) v.row(0)[words - 1] &= (~uint64_t(0)) >> (64 - (cols & 63));
+            if (!v.row_is_zero(0)) break;
+        }
+        for (int i = 0; i < rows; i++)
+            if (symplectic_ip(a.row(i), v.row(0), n)) {
+                uint64_t *u = a.row(i);
+                for (int w = 0; w < a.stride; w++) u[w] ^= v.row(0)[w];
+            }
+    }
+    return a;
+}
+
+}  // namespace sdb

@@ -1,0 +1,189 @@
+"""Freeze golden vectors from the REFERENCE library (oracle/_ref, built from
+/root/reference/proj/src by oracle/Makefile). Run in the build container:
+
+    make -C oracle && python tests/golden/make_golden.py [--heavy]
+
+Writes small JSON fixtures next to this script. The GPU box never runs this
+(it has no /root/reference); tests only read the JSON.
+
+Matrices are stored one hex string per row: the row's bits as an integer,
+column c at bit c (little-endian), so ``int(h, 16) >> c & 1`` is entry c.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle as O  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def hexrows(m) -> list[str]:
+    m = np.asarray(m, dtype=np.uint8)
+    out = []
+    for row in m:
+        v = 0
+        for c in np.nonzero(row)[0]:
+            v |= 1 << int(c)
+        out.append(format(v, "x"))
+    return out
+
+
+def dump(name: str, obj) -> None:
+    path = os.path.join(OUT, name)
+    with open(path, "w") as f:
+        json.dump(obj, f, separators=(",", ":"), sort_keys=True)
+    print("wrote", path, os.path.getsize(path), "bytes", flush=True)
+
+
+def gammas_of(a):
+    img = O.ref_isometry_transform(a)
+    return [dict(matrix=hexrows(g["matrix"]), rank_deficit=g["rank_deficit"], pivots=g["pivots"])
+            for g in O.ref_information_sets(img)]
+
+
+def single_config(cid: int, workers: int, g_max: int = 0, with_best: bool = False) -> dict:
+    c = O.CONFIGS[cid]
+    n, k, seed = c["n"], c["k"], c["seed"]
+    a = O.generate(n, k, seed)
+    t0 = time.time()
+    if g_max:
+        lv = O.ref_isometry_levels(a, workers=workers, g_max=g_max, native=True)
+        res = dict(trace=lv["trace"], level_candidates=lv["level_candidates"], complete=False,
+                   levels_run=len(lv["trace"]), ref_level_seconds=lv["level_seconds"], ref_workers=workers,
+                   ref_build="native")
+    else:
+        r = O.ref_compute_distance(a, "saved_isometry", workers=workers)
+        res = dict(trace=r.trace, distance=r.distance, candidates=r.candidates, generations=r.generations,
+                   complete=True, ref_elapsed_seconds=r.elapsed_seconds, ref_workers=workers, ref_build="default")
+    if with_best:
+        b = O.ref_isometry_best(a, workers=1)
+        res["best"] = hexrows([b["best"]])[0]
+        res["best_len"] = int(len(b["best"]))
+    res.update(config=cid, n=n, k=k, seed=seed, transvections=4 * n, normalizer=hexrows(a), gammas=gammas_of(a),
+               wall_seconds=time.time() - t0)
+    return res
+
+
+def batch_config() -> dict:
+    c = O.CONFIGS[3]
+    n, k = c["n"], c["k"]
+    codes = []
+    hist: dict = {}
+    for s in c["seeds"]:
+        a = O.generate(n, k, s)
+        r = O.ref_compute_distance(a, "saved_isometry", workers=1)
+        codes.append(dict(seed=s, distance=r.distance, trace=r.trace, candidates=r.candidates))
+        hist[r.distance] = hist.get(r.distance, 0) + 1
+    return dict(config=3, n=n, k=k, seeds=[c["seeds"][0], c["seeds"][-1]], codes=codes,
+                histogram={str(d): v for d, v in sorted(hist.items())})
+
+
+def reference_kats() -> dict:
+    """Instances from the reference's own tests, reproduced through its own
+    random_stabilizer (mt19937_64) and answered by its own algorithms."""
+    cases = []
+    # proj/tests/test_distance.cpp:122-125 mid-size instances (oracle agreement)
+    for n, k, seed in [(16, 1, 11), (18, 2, 12), (20, 0, 13), (22, 2, 14)]:
+        a = O.ref_random_stabilizer(n, k, seed)
+        iso = O.ref_compute_distance(a, "saved_isometry")
+        brute = O.ref_compute_distance(a, "brute_force")
+        cases.append(dict(src="test_distance.cpp:122-125", n=n, k=k, seed=seed, normalizer=hexrows(a),
+                          distance=iso.distance, brute=brute.distance, trace=iso.trace, candidates=iso.candidates))
+    # proj/tests/acceptance.cpp:124-157 criterion 3 sweep: seeds 10000 + 97*i
+    count = 0
+    for rep in range(3):
+        for n in range(4, 13):
+            for k in range(0, n + 1):
+                seed = 10000 + 97 * count
+                count += 1
+                a = O.ref_random_stabilizer(n, k, seed)
+                iso = O.ref_compute_distance(a, "saved_isometry")
+                brute = O.ref_compute_distance(a, "brute_force")
+                cases.append(dict(src="acceptance.cpp:124-157", n=n, k=k, seed=seed, normalizer=hexrows(a),
+                                  distance=iso.distance, brute=brute.distance, trace=iso.trace,
+                                  candidates=iso.candidates))
+    # proj/tests/acceptance.cpp:56-79 worked 3x4 example; test_distance.cpp:57-64 (I_5 | 0)
+    ex = np.array([[1, 0, 0, 1], [0, 1, 1, 0], [0, 0, 1, 1]], dtype=np.uint8)
+    r = O.ref_compute_distance(ex, "saved_isometry")
+    cases.append(dict(src="acceptance.cpp:56-79", n=2, k=1, seed=None, normalizer=hexrows(ex), distance=r.distance,
+                      brute=O.ref_compute_distance(ex, "brute_force").distance, trace=r.trace,
+                      candidates=r.candidates))
+    ident = np.zeros((5, 10), dtype=np.uint8)
+    for i in range(5):
+        ident[i, i] = 1
+    r = O.ref_compute_distance(ident, "saved_isometry")
+    cases.append(dict(src="test_distance.cpp:57-64", n=5, k=0, seed=None, normalizer=hexrows(ident),
+                      distance=r.distance, brute=O.ref_compute_distance(ident, "brute_force").distance,
+                      trace=r.trace, candidates=r.candidates))
+    return dict(cases=cases)
+
+
+def engine_kats() -> dict:
+    """Singleton-package run_bz cases in both weight modes across word boundaries, the
+    shape of proj/tests/test_engine.cpp:121-161 (n 60..79, 5 rows), inputs from a seeded
+    numpy generator, answers from the reference's run_bz."""
+    rng = np.random.default_rng(103)
+    cases = []
+    for it in range(6):
+        n = 60 + int(rng.integers(0, 20))
+        m = rng.integers(0, 2, size=(5, 2 * n), dtype=np.uint8)
+        sym = O.ref_run_bz_singleton(m, "symplectic")
+        img = O.ref_isometry_transform(m)
+        ham = O.ref_run_bz_singleton(img, "hamming")
+        cases.append(dict(src="test_engine.cpp:121-161", n=n, matrix=hexrows(m), symplectic=dict(
+            trace=sym["trace"], upper=sym["upper"], generation=sym["generation"], candidates=sym["candidates"]),
+            hamming=dict(trace=ham["trace"], upper=ham["upper"], generation=ham["generation"],
+                         candidates=ham["candidates"])))
+    # planted d=1 at n=70 (test_engine.cpp:163-182): scrambled (I_n | 0)
+    n = 70
+    a = np.zeros((n, 2 * n), dtype=np.uint8)
+    for i in range(n):
+        a[i, i] = 1
+    for _ in range(400):
+        r1, r2 = (int(x) for x in rng.integers(0, n, size=2))
+        if r1 != r2:
+            a[r2] ^= a[r1]
+    r = O.ref_compute_distance(a, "saved_isometry")
+    cases.append(dict(src="test_engine.cpp:163-182", n=n, planted=hexrows(a), distance=r.distance, trace=r.trace))
+    # filtered singleton runs with the reference's exhaustion error (test_engine.cpp:260-269)
+    return dict(cases=cases)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--heavy", action="store_true", help="also config 4 (full) and config 5 (g<=8)")
+    ap.add_argument("--workers", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    only = set(args.only.split(",")) if args.only else None
+
+    def want(x):
+        return only is None or x in only
+
+    if want("c1"):
+        dump("config1.json", single_config(1, 1, with_best=True))
+    if want("c2"):
+        dump("config2.json", single_config(2, args.workers, with_best=True))
+    if want("c3"):
+        dump("config3.json", batch_config())
+    if want("kats"):
+        dump("reference_kats.json", reference_kats())
+    if want("engine"):
+        dump("engine_kats.json", engine_kats())
+    if args.heavy and want("c4"):
+        dump("config4.json", single_config(4, args.workers))
+    if args.heavy and want("c5"):
+        dump("config5_g8.json", single_config(5, args.workers, g_max=8))
+
+
+if __name__ == "__main__":
+    main()

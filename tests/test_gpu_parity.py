@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA enumeration path (through the C ABI) against the golden fixtures
+frozen from the reference and against the oracle, on the BASELINE configs and the
+reference's own test instances. Bit-exact: distance, (g, L, U) trace, candidate counts,
+best codeword."""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import hex_to_mat, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def tr(rep):
+    return [e.astuple() for e in rep.bounds_trace]
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("name", ["config1.json", "config2.json"])
+def test_small_configs_bit_exact(gpu, name, kernel):
+    gd = load_golden(name)
+    a = hex_to_mat(gd["normalizer"], 2 * gd["n"])
+    rep, best = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel), return_best=True)
+    assert rep.distance == gd["distance"]
+    assert tr(rep) == [tuple(t) for t in gd["trace"]]
+    assert rep.candidates_enumerated == gd["candidates"]
+    assert rep.generations == gd["generations"]
+    assert rep.complete
+    # BoundsState::best of the single-worker reference = first minimal candidate in visiting order
+    assert (best == hex_to_mat([gd["best"]], gd["best_len"])[0]).all()
+
+
+def test_config4_bit_exact(gpu):
+    gd = load_golden("config4.json")
+    a = hex_to_mat(gd["normalizer"], 2 * gd["n"])
+    rep = gpu.saved_isometry(a)
+    assert rep.distance == gd["distance"] == 10
+    assert tr(rep) == [tuple(t) for t in gd["trace"]]
+    assert rep.candidates_enumerated == gd["candidates"]
+
+
+def test_config5_first_eight_levels_bit_exact(gpu):
+    gd = load_golden("config5_g8.json")
+    a = hex_to_mat(gd["normalizer"], 2 * gd["n"])
+    rep = gpu.saved_isometry(a, gpu.RunOptions(max_generation=8))
+    assert not rep.complete
+    assert tr(rep) == [tuple(t) for t in gd["trace"]]
+    assert rep.candidates_enumerated == sum(gd["level_candidates"])
+
+
+def test_batch_config3_bit_exact(gpu):
+    gd = load_golden("config3.json")
+    codes = [gpu.generate_code(gd["n"], gd["k"], c["seed"]) for c in gd["codes"]]
+    res = gpu.saved_isometry_batch(codes)
+    assert (res.statuses == 0).all()
+    assert [int(x) for x in res.distances] == [c["distance"] for c in gd["codes"]]
+    for got, c in zip(res.traces, gd["codes"]):
+        assert got == [tuple(t) for t in c["trace"]]
+
+
+def test_reference_kats(gpu):
+    gd = load_golden("reference_kats.json")
+    for case in gd["cases"]:
+        a = hex_to_mat(case["normalizer"], 2 * case["n"])
+        rep = gpu.saved_isometry(a)
+        assert rep.distance == case["distance"] == case["brute"], case
+        assert tr(rep) == [tuple(t) for t in case["trace"]], case
+        assert rep.candidates_enumerated == case["candidates"], case
+
+
+def test_reference_kats_batched(gpu):
+    gd = load_golden("reference_kats.json")
+    by_shape = {}
+    for case in gd["cases"]:
+        by_shape.setdefault((case["n"], case["k"]), []).append(case)
+    for (n, k), cases in by_shape.items():
+        mats = [hex_to_mat(c["normalizer"], 2 * n) for c in cases]
+        res = gpu.saved_isometry_batch(mats)
+        assert [int(x) for x in res.distances] == [c["distance"] for c in cases]
+        assert res.traces == [[tuple(t) for t in c["trace"]] for c in cases]
+
+
+def test_engine_singleton_kats_both_modes(gpu):
+    # proj/tests/test_engine.cpp:121-161 shapes, answers from the reference's run_bz
+    gd = load_golden("engine_kats.json")
+    for case in gd["cases"]:
+        if "matrix" not in case:
+            continue
+        n = case["n"]
+        m = hex_to_mat(case["matrix"], 2 * n)
+        sym = gpu.run_bz([gpu.singleton_gamma(m, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.disabled())
+        assert sym.trace == [tuple(t) for t in case["symplectic"]["trace"]]
+        assert sym.upper == case["symplectic"]["upper"]
+        assert sym.candidates_enumerated == case["symplectic"]["candidates"]
+        img = gpu.isometry_transform(m)
+        ham = gpu.run_bz([gpu.singleton_gamma(img, gpu.WeightMode.hamming)], gpu.AdmissibilityFilter.disabled())
+        assert ham.trace == [tuple(t) for t in case["hamming"]["trace"]]
+        assert ham.upper == case["hamming"]["upper"]
+        # general Hamming layout (not an isometry image): shuffle the columns
+        perm = np.random.default_rng(n).permutation(3 * n)
+        ham2 = gpu.run_bz([gpu.singleton_gamma(img[:, perm], gpu.WeightMode.hamming)],
+                          gpu.AdmissibilityFilter.disabled())
+        assert ham2.trace == ham.trace
+
+
+def test_planted_distance_one_wide(gpu):
+    # proj/tests/test_engine.cpp:163-182: scrambled (I_70 | 0), three words per half
+    gd = load_golden("engine_kats.json")
+    case = [c for c in gd["cases"] if "planted" in c][0]
+    a = hex_to_mat(case["planted"], 2 * case["n"])
+    rep = gpu.saved_isometry(a)
+    assert rep.distance == 1 == case["distance"]
+    assert tr(rep) == [tuple(t) for t in case["trace"]]
+
+
+def test_oracle_agreement_random_instances(gpu):
+    rng = np.random.default_rng(73)
+    for _ in range(30):
+        n = int(rng.integers(2, 30))
+        k = int(rng.integers(0, n + 1))
+        a = gpu.generate_code(n, k, int(rng.integers(1, 1 << 40)))
+        mine = gpu.saved_isometry(a)
+        ref = O.run_levels(a, threads=4)
+        assert tr(mine) == ref["trace"]
+        assert 2 * mine.distance == ref["upper"]
+        if a.shape[0] <= 22:
+            assert mine.distance == O.brute_force(a)
+
+
+def test_filter_off_and_self_dual(gpu):
+    # k = 0: filter disabled by construction (engine.cpp:19); dual_filter=False: plain minimum
+    ident = np.zeros((5, 10), dtype=np.uint8)
+    for i in range(5):
+        ident[i, i] = 1
+    assert gpu.saved_isometry(ident).distance == 1
+    a = gpu.generate_code(16, 3, 99)
+    plain = gpu.saved_isometry(a, gpu.RunOptions(dual_filter=False))
+    ref = O.run_levels(a, dual_filter=False)
+    assert tr(plain) == ref["trace"]
+    filt = gpu.saved_isometry(a)
+    assert plain.distance <= filt.distance
+
+
+def test_worked_example_and_errors(gpu):
+    ex = np.array([[1, 0, 0, 1], [0, 1, 1, 0], [0, 0, 1, 1]], dtype=np.uint8)
+    assert gpu.saved_isometry(ex).distance == 1
+    # raw matrix as singleton packages stops at 2 (test_engine.cpp:213-218)
+    plain = gpu.run_bz([gpu.singleton_gamma(ex, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.for_rows(ex, 1))
+    assert plain.upper == 2 and plain.generation == 1
+    # exhaustion without an admissible codeword (test_engine.cpp:260-269)
+    m = np.array([[1, 0, 0, 0]], dtype=np.uint8)
+    with pytest.raises(gpu.InternalError):
+        gpu.run_bz([gpu.singleton_gamma(m, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.for_rows(m, 1))
+    # malformed calls (test_engine.cpp:271-285)
+    g2 = gpu.singleton_gamma(np.array([[1, 0, 0, 1]]), gpu.WeightMode.symplectic)
+    g3 = gpu.singleton_gamma(np.array([[1, 0, 0, 1, 1, 1]]), gpu.WeightMode.symplectic)
+    with pytest.raises(ValueError):
+        gpu.run_bz([], gpu.AdmissibilityFilter.disabled())
+    with pytest.raises(ValueError):
+        gpu.run_bz([g2, g3], gpu.AdmissibilityFilter.disabled())
+    with pytest.raises(ValueError):
+        gpu.run_bz([g2], gpu.AdmissibilityFilter.for_rows(np.array([[1, 0, 0, 1, 1, 1]]), 1))
+    # validation gate (test_distance.cpp:93-100)
+    with pytest.raises(gpu.ValidationError):
+        gpu.saved_isometry(np.array([[1, 0, 0, 1], [1, 0, 0, 1], [0, 0, 1, 1]]))
+
+
+def test_visit_count_single_candidate(gpu):
+    # test_engine.cpp:66-78: g = n_p on all-singleton packages visits one candidate
+    m = np.eye(6, dtype=np.uint8)
+    st = gpu.run_bz([gpu.singleton_gamma(m, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.disabled())
+    assert st.report.candidates_visited == st.candidates_enumerated

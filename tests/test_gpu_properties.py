@@ -1,0 +1,79 @@
+"""GPU: size-independent properties at full sizes, sharding invariance and the
+device-resident plan."""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def tr(rep):
+    return [e.astuple() for e in rep.bounds_trace]
+
+
+def test_trace_properties_on_configs(gpu):
+    for cid in (1, 2, 4):
+        c = gpu.CONFIGS[cid]
+        a = gpu.generate_code(c["n"], c["k"], c["seed"])
+        rep = gpu.saved_isometry(a)
+        t = tr(rep)
+        assert all(t[i + 1][1] >= t[i][1] and t[i + 1][2] <= t[i][2] for i in range(len(t) - 1))
+        assert t[-1][2] % 2 == 0 and t[-1][2] == 2 * rep.distance
+        assert t[-1][1] >= t[-1][2]
+        assert rep.candidates_visited == rep.candidates_enumerated
+
+
+class _ThreadAllreduce:
+    """In-process stand-in for the NCCL/gloo min-allreduce: ranks are threads."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.lock = threading.Lock()
+        self.vals = {}
+
+    def fn_for(self, rank):
+        def fn(values):
+            with self.lock:
+                self.vals[rank] = values.copy()
+            self.barrier.wait()
+            out = np.minimum.reduce([self.vals[r] for r in range(self.world)])
+            self.barrier.wait()
+            return out
+        return fn
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_levels_match_single(gpu, world):
+    c = gpu.CONFIGS[2]
+    a = gpu.generate_code(c["n"], c["k"], c["seed"])
+    single, best1 = gpu.saved_isometry(a, return_best=True)
+    ar = _ThreadAllreduce(world)
+    out = [None] * world
+
+    def run(r):
+        out[r] = gpu.saved_isometry(a, gpu.RunOptions(rank=r, world=world, allreduce_min=ar.fn_for(r)),
+                                    return_best=True)
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for rep, best in out:
+        assert tr(rep) == tr(single)
+        assert rep.distance == single.distance
+        assert (best == best1).all()
+    assert sum(rep.candidates_visited for rep, _ in out) == single.candidates_visited
+
+
+def test_plan_reuse_is_deterministic(gpu):
+    c = gpu.CONFIGS[2]
+    a = gpu.generate_code(c["n"], c["k"], c["seed"])
+    with gpu.Plan(a) as plan:
+        r1 = plan.run()
+        r2 = plan.run()
+    assert tr(r1) == tr(r2)
+    assert r1.distance == 7
+    assert len(r1.level_seconds) == len(r1.bounds_trace)
