@@ -14,6 +14,12 @@
 
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define SDB_HD __host__ __device__
+#else
+#define SDB_HD
+#endif
+
 namespace sdb {
 
 constexpr int kMaxW = 8;         // u32 words per half: n <= 256
@@ -54,7 +60,30 @@ struct LevelLaunch {
 int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, int num_sms);
 
 // One level, all matrices, head x tail tile kernel (large levels).
-struct TilePlan;
+//
+// Every g-subset S of the N rows splits at b = the smallest of its last t elements into a
+// head (h = g - t elements, all < b) and a tail ({b} plus t-1 elements > b). For fixed
+// (Gamma j, b) the candidates are the outer product Heads_b x Tails_b, with
+// |Heads_b| = C(b, h) (colex ranks of h-subsets of [0, b)) and |Tails_b| = C(N-1-b, t-1).
+// A work unit is (j, b, head block of head_block(W) heads, tail chunk of kTailChunk tails):
+// the CTA stages the tail chunk in shared memory, each lane holds heads_per_lane(W) heads in
+// registers and streams the tails as warp-uniform broadcast loads, so one candidate is
+// one XOR of two precomputed sums fused with the OR (2 LOP3) plus one POPC.
+constexpr int kTileThreads = 256;
+// heads held in registers per lane (2W words each); fewer for wide rows to avoid spills
+SDB_HD constexpr int heads_per_lane(int W) { return W <= 3 ? 8 : (W <= 5 ? 4 : 2); }
+SDB_HD constexpr int head_block(int W) { return kTileThreads * heads_per_lane(W); }
+constexpr int kTailChunk = 1024;
+
+struct TilePlan {
+    int g, t, h;
+    unsigned int thr0;              // candidates with weight <= thr0 are considered (U - 1)
+    int nb;                         // number of boundaries b in [h, N - t]
+    const unsigned long long *cum;  // [G * nb + 1] cumulative unit counts over (j, b)
+    unsigned long long *counter;    // dynamic unit dispenser (starts at unit_begin)
+    unsigned long long unit_begin, unit_end;
+    unsigned long long per_gamma;   // C(N, g): lexicographic-rank base
+};
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms);
 
 // Batch: one code per CTA, the whole level loop on the device.

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -160,8 +161,9 @@ void Plan::upload() {
     const size_t b_rows = align256(h_rows_.size() * 4), b_syn = align256(std::max<size_t>(h_syn_.size(), 1) * 8),
                  b_binom = align256(h_binom_.size() * 8),
                  b_state = align256(sizeof(LevelState) + size_t(max_weight_ + 1) * 8);
+    const size_t b_cum = align256((size_t(G_) * (N_ + 1) + 2) * 8);
     const auto t0 = std::chrono::steady_clock::now();
-    check_cuda(cudaMalloc(&d_mem_, b_rows + b_syn + b_binom + b_state), "cudaMalloc");
+    check_cuda(cudaMalloc(&d_mem_, b_rows + b_syn + b_binom + b_state + b_cum), "cudaMalloc");
     unsigned char *base = static_cast<unsigned char *>(d_mem_);
     check_cuda(cudaMemcpyAsync(base, h_rows_.data(), h_rows_.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D rows");
     if (!h_syn_.empty())
@@ -177,6 +179,9 @@ void Plan::upload() {
     pd_.binom = reinterpret_cast<const unsigned long long *>(base + b_rows + b_syn);
     pd_.state = reinterpret_cast<LevelState *>(base + b_rows + b_syn + b_binom);
     pd_.key_by_w = reinterpret_cast<unsigned long long *>(base + b_rows + b_syn + b_binom + sizeof(LevelState));
+    d_cum_ = reinterpret_cast<unsigned long long *>(base + b_rows + b_syn + b_binom + b_state);
+    d_counter_ = d_cum_ + size_t(G_) * (N_ + 1) + 1;
+    h_cum_.assign(size_t(G_) * (N_ + 1) + 2, 0);
     pd_.G = G_;
     pd_.N = N_;
     pd_.W = W_;
@@ -187,6 +192,38 @@ void Plan::upload() {
     h_state_.assign(sizeof(LevelState) + size_t(max_weight_ + 1) * 8, 0);
     if (problem_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
         throw InvalidArgument("problem too large for shared-memory staging");
+}
+
+size_t tile_smem_bytes(int G, int N, int W, int SW, int BK);
+
+int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel) {
+    if (forced_kernel == 1 || g < 2) return 0;
+    const double HBk = head_block(W), Hl = heads_per_lane(W);
+    const double total = double(per_gamma) * G;
+    if (forced_kernel != 2 && total < double(1 << 22)) return 0;
+    // relative lane-cycle costs: walk ~12 per candidate; tile ~1 per candidate plus
+    // per-unit head generation (unrank + successors), tail staging and scheduling
+    const double walk_cost = total * 12.0;
+    double best = 0;
+    int best_t = 0;
+    for (int t = 1; t < g; t++) {
+        const int h = g - t;
+        double cost = 0;
+        for (int b = h; b <= N - t; b++) {
+            const double Hb = double(binom_u64(b, h)), Tb = double(binom_u64(N - 1 - b, t - 1));
+            const double nH = std::ceil(Hb / HBk), nT = std::ceil(Tb / kTailChunk);
+            const double tc = Tb / nT;
+            const double heads_last = Hb - (nH - 1) * HBk;
+            const double warps_full = kTileThreads / 32, warps_last = std::ceil(heads_last / (32.0 * Hl));
+            const double warps = ((nH - 1) * warps_full + warps_last) / nH;
+            const double unit = 32.0 * (warps * (Hl * tc + 100.0) + warps_full * (0.2 * tc + 60.0));
+            cost += nH * nT * unit;
+        }
+        cost *= G;
+        if (best_t == 0 || cost < best) { best = cost; best_t = t; }
+    }
+    if (forced_kernel == 2) return best_t;
+    return best < walk_cost ? best_t : 0;
 }
 
 long long Plan::lower_bound(int g) const {
@@ -236,7 +273,40 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         check_cuda(cudaMemsetAsync(pd_.state, 0xFF, h_state_.size(), stream_), "memset state");
         check_cuda(cudaMemsetAsync(&pd_.state->visited, 0, 8, stream_), "memset visited");
         check_cuda(cudaEventRecord(ev0_, stream_), "event");
-        const int nl = launch_walk_level(pd_, LL, stream_, num_sms_);
+        const int t = choose_tile_t(G_, N_, g, W_, per, opts_.kernel);
+        int nl;
+        if (t == 0) {
+            nl = launch_walk_level(pd_, LL, stream_, num_sms_);
+        } else {
+            TilePlan tp{};
+            tp.g = g;
+            tp.t = t;
+            tp.h = g - t;
+            tp.thr0 = unsigned(U - 1);
+            tp.nb = N_ - t - tp.h + 1;
+            tp.per_gamma = per;
+            unsigned long long acc = 0;
+            for (int j = 0; j < G_; j++)
+                for (int b = tp.h; b <= N_ - t; b++) {
+                    h_cum_[size_t(j) * tp.nb + (b - tp.h)] = acc;
+                    const unsigned long long Hb = binom_u64(b, tp.h), Tb = binom_u64(N_ - 1 - b, t - 1);
+                    acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + kTailChunk - 1) / kTailChunk);
+                }
+            h_cum_[size_t(G_) * tp.nb] = acc;
+            tp.unit_begin = (unsigned long long)((unsigned __int128)acc * rank / world);
+            tp.unit_end = (unsigned long long)((unsigned __int128)acc * (rank + 1) / world);
+            h_cum_[size_t(G_) * tp.nb + 1] = tp.unit_begin;  // staged counter start
+            check_cuda(cudaMemcpyAsync(d_cum_, h_cum_.data(), (size_t(G_) * tp.nb + 1) * 8, cudaMemcpyHostToDevice,
+                                       stream_),
+                       "H2D unit table");
+            check_cuda(cudaMemcpyAsync(d_counter_, &h_cum_[size_t(G_) * tp.nb + 1], 8, cudaMemcpyHostToDevice, stream_),
+                       "H2D unit counter");
+            tp.cum = d_cum_;
+            tp.counter = d_counter_;
+            if (tile_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
+                throw InvalidArgument("problem too large for shared-memory staging");
+            nl = launch_tile_level(pd_, tp, stream_, num_sms_);
+        }
         if (nl < 0) throw InvalidArgument("unsupported row width");
         launches += nl;
         check_cuda(cudaGetLastError(), "walk kernel launch");

@@ -72,7 +72,14 @@ class Plan {
     void *d_mem_ = nullptr;
     ProblemDev pd_{};
     std::vector<unsigned char> h_state_;
+    unsigned long long *d_cum_ = nullptr;      // [G * (N + 1) + 1] tile unit table
+    unsigned long long *d_counter_ = nullptr;  // tile unit dispenser
+    std::vector<unsigned long long> h_cum_;
 };
+
+// Host cost model for one level: 0 = lexicographic-walk kernel, else the tail size t of
+// the head x tail tile kernel. Exposed for tests.
+int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel);
 
 // Saturating binomial table (N+1) x BK.
 std::vector<unsigned long long> binom_table(int N, int BK);

@@ -213,6 +213,271 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     }
 }
 
+
+// ---------------------------------------------------------------- tile: heads x tails
+
+// colex unrank of rho into an m-subset of [0, lim), ascending into e[0..m-1]
+__device__ __forceinline__ void unrank_colex(unsigned long long rho, int m, int lim, const unsigned long long *binom,
+                                             int BK, int *e) {
+    int c = lim - 1;
+    for (int i = m; i >= 1; i--) {
+        unsigned long long v;
+        while ((v = binom_at(binom, BK, c, i)) > rho) c--;
+        e[i - 1] = c;
+        rho -= v;
+        c--;
+    }
+}
+
+// lexicographic rank of ascending c[0..g-1] among g-subsets of [0, N): the reference's
+// visiting order inside one generation (engine.cpp:202-219)
+__device__ __forceinline__ unsigned long long lexrank(const int *c, int g, int N, const unsigned long long *binom,
+                                                      int BK, unsigned long long per) {
+    unsigned long long s = 0;
+    for (int i = 1; i <= g; i++) s += binom_at(binom, BK, N - 1 - c[g - i], i);
+    return per - 1 - s;
+}
+
+// Rare path: a candidate whose exact weight passed the threshold. Rebuilds its element
+// list from the head rank and the tail rank, applies the admissibility syndrome and
+// publishes (weight, key). Returns the updated threshold.
+__device__ __noinline__ unsigned tile_publish(const ProblemDev p, const TilePlan tp, int j, int b,
+                                              unsigned long long head_rank, unsigned long long tail_rank,
+                                              const unsigned long long *tsyn, unsigned w, unsigned thrH) {
+    const int N = p.N, h = tp.h, t = tp.t;
+    int c[kMaxLevel];
+    unrank_colex(head_rank, h, b, p.binom, p.BK, c);
+    c[h] = b;
+    unrank_colex(tail_rank, t - 1, N - 1 - b, p.binom, p.BK, c + h + 1);
+    for (int k = h + 1; k < h + t; k++) c[k] += b + 1;
+    if (p.SW) {
+        const unsigned long long *syn = p.syn + (size_t)j * N * p.SW;
+        bool adm = false;
+        for (int s = 0; s < p.SW; s++) {
+            unsigned long long x = tsyn[s];
+            for (int k = 0; k < h; k++) x ^= syn[c[k] * p.SW + s];
+            adm |= x != 0;
+        }
+        if (!adm) return thrH;
+    }
+    const unsigned long long key =
+        ((unsigned long long)j << kKeyRankBits) | lexrank(c, tp.g, N, p.binom, p.BK, tp.per_gamma);
+    atomicMin(&p.state->wmin, w);
+    atomicMin(&p.key_by_w[w], key);
+    return w;
+}
+
+// OR-fold of the W words of (x ^ tx) | (z ^ tz): popc of the fold is a lower bound on the
+// candidate's weight (exact for W = 1), one POPC per candidate whatever W is.
+template <int W>
+__device__ __forceinline__ uint32_t fold(const uint32_t (&hx)[W], const uint32_t (&hz)[W], const uint32_t *t) {
+    uint32_t u = (hx[0] ^ t[0]) | (hz[0] ^ t[W]);
+#pragma unroll
+    for (int w = 1; w < W; w++) u |= (hx[w] ^ t[w]) | (hz[w] ^ t[W + w]);
+    return u;
+}
+
+template <int W>
+__device__ __forceinline__ unsigned exact_weight(const uint32_t (&hx)[W], const uint32_t (&hz)[W], const uint32_t *t) {
+    unsigned s = 0;
+#pragma unroll
+    for (int w = 0; w < W; w++) s += __popc((hx[w] ^ t[w]) | (hz[w] ^ t[W + w]));
+    return s;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, TilePlan tp) {
+    constexpr int H = heads_per_lane(W);
+    constexpr int HB = head_block(W);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int rowlen = 2 * W;
+    const int G = p.G, N = p.N, SW = p.SW;
+    const int nrow_words = G * N * rowlen;
+    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem);
+    unsigned long long *s_binom =
+        reinterpret_cast<unsigned long long *>(smem + ((nrow_words * 4 + 15) & ~15));
+    const int nbinom = (N + 1) * p.BK;
+    unsigned long long *s_syn = s_binom + nbinom;
+    const int nsyn = G * N * SW;
+    // tail chunk: 2W words per tail (x block then z block), one spare tail for odd counts
+    uint32_t *s_tail = reinterpret_cast<uint32_t *>(s_syn + nsyn + (nsyn & 1));
+    unsigned long long *s_tsyn =
+        reinterpret_cast<unsigned long long *>(s_tail + (((kTailChunk + 1) * rowlen + 3) & ~3));
+    __shared__ unsigned long long s_unit;
+    __shared__ unsigned long long s_visited;
+    for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
+    for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[i];
+    for (int i = threadIdx.x; i < nsyn; i += blockDim.x) s_syn[i] = p.syn[i];
+    if (threadIdx.x == 0) s_visited = 0;
+
+    const int t = tp.t, h = tp.h;
+    const unsigned sshift = p.scale == 2 ? 1u : 0u;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned thrH = min(tp.thr0, *(volatile unsigned int *)&p.state->wmin);
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_unit = atomicAdd(tp.counter, 1ull);
+        __syncthreads();
+        const unsigned long long unit = s_unit;
+        if (unit >= tp.unit_end) break;
+        // (j, b): the last q with cum[q] <= unit
+        int lo = 0, hi = G * tp.nb - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(tp.cum + mid) <= unit) lo = mid; else hi = mid - 1;
+        }
+        const int j = lo / tp.nb, b = h + lo % tp.nb;
+        const unsigned long long u = unit - __ldg(tp.cum + lo);
+        const unsigned long long Hb = binom_at(s_binom, p.BK, b, h);
+        const unsigned long long Tb = binom_at(s_binom, p.BK, N - 1 - b, t - 1);
+        const unsigned long long nT = (Tb + kTailChunk - 1) / kTailChunk;
+        const unsigned long long hc = u / nT, tc = u % nT;
+        const unsigned long long t0 = tc * kTailChunk;
+        const int tcount = int(min((unsigned long long)kTailChunk, Tb - t0));
+        const uint32_t *grows = s_rows + j * N * rowlen;
+        const unsigned long long *gsyn = s_syn + j * N * SW;
+
+        // stage the tail chunk: {b} + colex (t-1)-subsets of (b, N)
+        for (int i = threadIdx.x; i < tcount; i += blockDim.x) {
+            int e[kMaxLevel];
+            unrank_colex(t0 + i, t - 1, N - 1 - b, s_binom, p.BK, e);
+            uint32_t acc[2 * W];
+#pragma unroll
+            for (int w = 0; w < 2 * W; w++) acc[w] = grows[b * rowlen + w];
+            for (int k = 0; k < t - 1; k++) xor_row<W>(acc, grows + (b + 1 + e[k]) * rowlen);
+            for (int s = 0; s < SW; s++) {
+                unsigned long long x = gsyn[b * SW + s];
+                for (int k = 0; k < t - 1; k++) x ^= gsyn[(b + 1 + e[k]) * SW + s];
+                s_tsyn[i * SW + s] = x;
+            }
+#pragma unroll
+            for (int w = 0; w < 2 * W; w++) s_tail[i * rowlen + w] = acc[w];
+            if (i == tcount - 1 && (tcount & 1))  // pad odd counts with a duplicate
+#pragma unroll
+                for (int w = 0; w < 2 * W; w++) s_tail[(i + 1) * rowlen + w] = acc[w];
+        }
+        __syncthreads();
+
+        // this lane's heads: H consecutive colex ranks of h-subsets of [0, b)
+        const unsigned long long hbase = hc * HB + (unsigned long long)warp * (32 * H) + lane * H;
+        const int nvalid = hbase >= Hb ? 0 : int(min((unsigned long long)H, Hb - hbase));
+        if (threadIdx.x == 0) {
+            const unsigned long long blk = min((unsigned long long)HB, Hb - hc * HB);
+            s_visited += blk * (unsigned long long)tcount;
+        }
+        if (!__any_sync(0xffffffffu, nvalid > 0)) continue;
+        uint32_t hx[H][W], hz[H][W];
+        {
+            int e[kMaxLevel];
+            uint32_t x[W], z[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) x[w] = z[w] = 0;
+            if (nvalid > 0) {
+                unrank_colex(hbase, h, b, s_binom, p.BK, e);
+                for (int k = 0; k < h; k++)
+#pragma unroll
+                    for (int w = 0; w < W; w++) {
+                        x[w] ^= grows[e[k] * rowlen + w];
+                        z[w] ^= grows[e[k] * rowlen + W + w];
+                    }
+            } else {
+                // lanes without heads: all-ones fold, never passes the threshold check below
+#pragma unroll
+                for (int w = 0; w < W; w++) x[w] = z[w] = 0xffffffffu;
+            }
+#pragma unroll
+            for (int i = 0; i < H; i++) {
+                if (i > 0 && i < nvalid) {
+                    // colex successor: lowest element that can move up by one
+                    int q = 0;
+                    while (q < h - 1 && e[q] + 1 == e[q + 1]) q++;
+                    for (int k = 0; k <= q; k++)
+#pragma unroll
+                        for (int w = 0; w < W; w++) {
+                            x[w] ^= grows[e[k] * rowlen + w];
+                            z[w] ^= grows[e[k] * rowlen + W + w];
+                        }
+                    e[q]++;
+                    for (int k = 0; k < q; k++) e[k] = k;
+                    for (int k = 0; k <= q; k++)
+#pragma unroll
+                        for (int w = 0; w < W; w++) {
+                            x[w] ^= grows[e[k] * rowlen + w];
+                            z[w] ^= grows[e[k] * rowlen + W + w];
+                        }
+                }
+                // heads past the valid count repeat the last valid head (same candidates)
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    hx[i][w] = x[w];
+                    hz[i][w] = z[w];
+                }
+            }
+        }
+
+        unsigned thr0 = thrH >> sshift;
+        for (int ti = 0; ti < tcount; ti += 2) {
+            const uint32_t *ta = s_tail + ti * rowlen;
+            const uint32_t *tb = ta + rowlen;
+            unsigned m = 0xffffffffu;
+#pragma unroll
+            for (int i = 0; i < H; i++) {
+                const unsigned a = __popc(fold<W>(hx[i], hz[i], ta));
+                const unsigned c = __popc(fold<W>(hx[i], hz[i], tb));
+                m = min(m, min(a, c));
+            }
+            if (m <= thr0 && nvalid > 0) {
+                // rare: exact weights for this tail pair
+#pragma unroll
+                for (int i = 0; i < H; i++) {
+                    if (i < nvalid) {
+                        const unsigned wa = exact_weight<W>(hx[i], hz[i], ta) << sshift;
+                        if (wa <= thrH) {
+                            thrH = tile_publish(p, tp, j, b, hbase + i, t0 + ti, s_tsyn + ti * SW, wa, thrH);
+                            thr0 = thrH >> sshift;
+                        }
+                        const unsigned wb = exact_weight<W>(hx[i], hz[i], tb) << sshift;
+                        if (ti + 1 < tcount && wb <= thrH) {
+                            thrH = tile_publish(p, tp, j, b, hbase + i, t0 + ti + 1, s_tsyn + (ti + 1) * SW, wb,
+                                                thrH);
+                            thr0 = thrH >> sshift;
+                        }
+                    }
+                }
+            }
+        }
+        thrH = min(thrH, *(volatile unsigned int *)&p.state->wmin);
+    }
+    if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
+}
+
+size_t tile_smem(int G, int N, int W, int SW, int BK) {
+    size_t base = ((size_t(G) * N * 2 * W * 4 + 15) & ~size_t(15)) + size_t(N + 1) * BK * 8 + size_t(G) * N * SW * 8;
+    base += (size_t(G) * N * SW & 1) * 8;
+    base += size_t(((kTailChunk + 1) * 2 * W + 3) & ~3) * 4;
+    base += size_t(kTailChunk) * SW * 8;
+    return base;
+}
+
+template <int W>
+int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, int num_sms) {
+    const size_t smem = tile_smem(p.G, p.N, W, p.SW, p.BK);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<W>, kTileThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const unsigned long long units = tp.unit_end - tp.unit_begin;
+    unsigned long long blocks = (unsigned long long)num_sms * per_sm;
+    if (blocks > units) blocks = units;
+    if (blocks == 0) return 0;
+    tile_kernel<W><<<unsigned(blocks), kTileThreads, smem, st>>>(p, tp);
+    return 1;
+}
+
 size_t problem_smem(int G, int N, int W, int SW, int BK) {
     return ((size_t(G) * N * 2 * W * 4 + 15) & ~size_t(15)) + size_t(N + 1) * BK * 8 + size_t(G) * N * SW * 8;
 }
@@ -250,6 +515,22 @@ int launch_batch_impl(const BatchDev &b, cudaStream_t st) {
 }  // namespace
 
 size_t problem_smem_bytes(int G, int N, int W, int SW, int BK) { return problem_smem(G, N, W, SW, BK); }
+size_t tile_smem_bytes(int G, int N, int W, int SW, int BK) { return tile_smem(G, N, W, SW, BK); }
+
+int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (p.W) {
+        case 1: return launch_tile_impl<1>(p, tp, st, num_sms);
+        case 2: return launch_tile_impl<2>(p, tp, st, num_sms);
+        case 3: return launch_tile_impl<3>(p, tp, st, num_sms);
+        case 4: return launch_tile_impl<4>(p, tp, st, num_sms);
+        case 5: return launch_tile_impl<5>(p, tp, st, num_sms);
+        case 6: return launch_tile_impl<6>(p, tp, st, num_sms);
+        case 7: return launch_tile_impl<7>(p, tp, st, num_sms);
+        case 8: return launch_tile_impl<8>(p, tp, st, num_sms);
+    }
+    return -1;
+}
 
 int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, int num_sms) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -15,7 +15,7 @@ def tr(rep):
     return [e.astuple() for e in rep.bounds_trace]
 
 
-@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("kernel", [0, 1, 2])
 @pytest.mark.parametrize("name", ["config1.json", "config2.json"])
 def test_small_configs_bit_exact(gpu, name, kernel):
     gd = load_golden(name)
@@ -30,10 +30,11 @@ def test_small_configs_bit_exact(gpu, name, kernel):
     assert (best == hex_to_mat([gd["best"]], gd["best_len"])[0]).all()
 
 
-def test_config4_bit_exact(gpu):
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_config4_bit_exact(gpu, kernel):
     gd = load_golden("config4.json")
     a = hex_to_mat(gd["normalizer"], 2 * gd["n"])
-    rep = gpu.saved_isometry(a)
+    rep = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel))
     assert rep.distance == gd["distance"] == 10
     assert tr(rep) == [tuple(t) for t in gd["trace"]]
     assert rep.candidates_enumerated == gd["candidates"]
@@ -113,13 +114,17 @@ def test_planted_distance_one_wide(gpu):
     assert tr(rep) == [tuple(t) for t in case["trace"]]
 
 
-def test_oracle_agreement_random_instances(gpu):
+@pytest.mark.parametrize("kernel", [0, 1, 2])
+def test_oracle_agreement_random_instances(gpu, kernel):
     rng = np.random.default_rng(73)
     for _ in range(30):
         n = int(rng.integers(2, 30))
         k = int(rng.integers(0, n + 1))
         a = gpu.generate_code(n, k, int(rng.integers(1, 1 << 40)))
-        mine = gpu.saved_isometry(a)
+        mine, best = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel), return_best=True)
+        if kernel:
+            base, best0 = gpu.saved_isometry(a, return_best=True)
+            assert (best == best0).all()
         ref = O.run_levels(a, threads=4)
         assert tr(mine) == ref["trace"]
         assert 2 * mine.distance == ref["upper"]
@@ -170,3 +175,20 @@ def test_visit_count_single_candidate(gpu):
     m = np.eye(6, dtype=np.uint8)
     st = gpu.run_bz([gpu.singleton_gamma(m, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.disabled())
     assert st.report.candidates_visited == st.candidates_enumerated
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_engine_kats_forced_kernels(gpu, kernel):
+    gd = load_golden("engine_kats.json")
+    for case in gd["cases"]:
+        if "matrix" not in case:
+            continue
+        n = case["n"]
+        m = hex_to_mat(case["matrix"], 2 * n)
+        o = gpu.RunOptions(kernel=kernel)
+        sym = gpu.run_bz([gpu.singleton_gamma(m, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.disabled(),
+                         opts=o)
+        assert sym.trace == [tuple(t) for t in case["symplectic"]["trace"]]
+        ham = gpu.run_bz([gpu.singleton_gamma(gpu.isometry_transform(m), gpu.WeightMode.hamming)],
+                         gpu.AdmissibilityFilter.disabled(), opts=o)
+        assert ham.trace == [tuple(t) for t in case["hamming"]["trace"]]
