@@ -92,7 +92,8 @@ typedef struct {
     sdb_allreduce_min_fn allreduce_min;
     void *allreduce_ctx;
     int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel, 2 force the tile kernel */
-    int reserved[7];
+    void *stream;           /* cudaStream_t to run on (NULL: a private non-blocking stream) */
+    int reserved[6];
 } sdb_run_options;
 
 /* symdist::DistanceReport (distance.hpp:44-52) plus GPU-side measurements. */
@@ -115,7 +116,9 @@ typedef struct {
     int best_generation;                 /* level of the first minimal candidate (-1: none) */
     int best_gamma;                      /* its Gamma index */
     unsigned long long best_rank;        /* its lexicographic rank inside that level/Gamma */
-    int reserved[8];
+    unsigned long long h2d_bytes;        /* host->device bytes this call moved */
+    unsigned long long d2h_bytes;        /* device->host bytes this call moved */
+    int reserved[4];
 } sdb_report;
 
 void sdb_default_options(sdb_run_options *opts);

@@ -100,7 +100,7 @@ class _Options(C.Structure):
     _fields_ = [
         ("workers", C.c_int), ("validate", C.c_int), ("dual_filter", C.c_int), ("device", C.c_int),
         ("max_generation", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("allreduce_min", _ALLREDUCE),
-        ("allreduce_ctx", C.c_void_p), ("kernel", C.c_int), ("reserved", C.c_int * 7),
+        ("allreduce_ctx", C.c_void_p), ("kernel", C.c_int), ("stream", C.c_void_p), ("reserved", C.c_int * 6),
     ]
 
 
@@ -111,7 +111,8 @@ class _Report(C.Structure):
         ("trace_len", C.c_int), ("complete", C.c_int), ("upper", C.c_longlong),
         ("candidates_visited", C.c_ulonglong), ("prep_seconds", C.c_double), ("enum_seconds", C.c_double),
         ("n_gammas", C.c_int), ("kernel_launches", C.c_int), ("best_generation", C.c_int), ("best_gamma", C.c_int),
-        ("best_rank", C.c_ulonglong), ("reserved", C.c_int * 8),
+        ("best_rank", C.c_ulonglong), ("h2d_bytes", C.c_ulonglong), ("d2h_bytes", C.c_ulonglong),
+        ("reserved", C.c_int * 4),
     ]
 
 
@@ -227,6 +228,7 @@ class RunOptions:
     world: int = 1
     allreduce_min: Optional[Callable[[np.ndarray], np.ndarray]] = None
     kernel: int = 0  # 0 auto, 1 walk, 2 tile
+    stream: int = 0  # cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream); 0 = private
 
     def _c(self) -> tuple[_Options, object]:
         o = _Options()
@@ -238,6 +240,7 @@ class RunOptions:
         o.rank = self.rank
         o.world = self.world
         o.kernel = self.kernel
+        o.stream = self.stream or None
         keep = None
         if self.allreduce_min is not None:
             fn = self.allreduce_min
@@ -285,6 +288,8 @@ class DistanceReport:
     best_generation: int = -1
     best_gamma: int = -1
     best_rank: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
     level_seconds: list = field(default_factory=list)
 
     def trace_tuples(self):
@@ -301,7 +306,7 @@ def _report(r: _Report, tr, cap: int) -> DistanceReport:
         complete=bool(r.complete), upper=int(r.upper), candidates_visited=int(r.candidates_visited),
         prep_seconds=r.prep_seconds, enum_seconds=r.enum_seconds, n_gammas=r.n_gammas,
         kernel_launches=r.kernel_launches, best_generation=r.best_generation, best_gamma=r.best_gamma,
-        best_rank=int(r.best_rank))
+        best_rank=int(r.best_rank), h2d_bytes=int(r.h2d_bytes), d2h_bytes=int(r.d2h_bytes))
 
 
 _TRACE_CAP = 512

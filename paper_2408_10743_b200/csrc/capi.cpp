@@ -87,6 +87,7 @@ void saved_isometry_impl(const uint64_t *rows, int n_rows, int n_cols, int row_w
     if (f.enabled) f.rows = a;
     const auto tp = std::chrono::steady_clock::now();
     sdb::Plan plan(std::move(gammas), sdb::Mode::hamming, n, f, o);
+    rep->h2d_bytes = plan.upload_bytes;
     plan.run(rep, trace, trace_cap, best_out, nullptr);
     rep->prep_seconds = std::chrono::duration<double>(tp - t0).count() + plan.h2d_seconds;
     if (rep->complete && rep->upper % 2 != 0)

@@ -146,7 +146,7 @@ Plan::~Plan() {
     if (d_mem_) cudaFree(d_mem_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
-    if (stream_) cudaStreamDestroy(stream_);
+    if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -155,7 +155,12 @@ void Plan::upload() {
     device_ = opts_.device;
     check_cuda(cudaSetDevice(device_), "cudaSetDevice");
     check_cuda(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_), "cudaDeviceGetAttribute");
-    check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (opts_.stream) {
+        stream_ = static_cast<cudaStream_t>(opts_.stream);
+        own_stream_ = false;
+    } else {
+        check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
     check_cuda(cudaEventCreate(&ev0_), "cudaEventCreate");
     check_cuda(cudaEventCreate(&ev1_), "cudaEventCreate");
     const size_t b_rows = align256(h_rows_.size() * 4), b_syn = align256(std::max<size_t>(h_syn_.size(), 1) * 8),
@@ -174,6 +179,7 @@ void Plan::upload() {
                "H2D binom");
     check_cuda(cudaStreamSynchronize(stream_), "H2D sync");
     h2d_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    upload_bytes = h_rows_.size() * 4 + h_syn_.size() * 8 + h_binom_.size() * 8;
     pd_.rows = reinterpret_cast<const uint32_t *>(base);
     pd_.syn = reinterpret_cast<const unsigned long long *>(base + b_rows);
     pd_.binom = reinterpret_cast<const unsigned long long *>(base + b_rows + b_syn);
@@ -246,7 +252,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     if (world > 1 && !opts_.allreduce_min) throw InvalidArgument("world > 1 needs an allreduce_min callback");
     long long U = sentinel_, L = 1;
     int generation = 0, launches = 0;
-    unsigned long long candidates = 0, visited = 0;
+    unsigned long long candidates = 0, visited = 0, h2d = 0, d2h = 0;
     double enum_s = 0;
     int best_g = -1, best_j = -1;
     unsigned long long best_r = 0;
@@ -301,6 +307,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
                        "H2D unit table");
             check_cuda(cudaMemcpyAsync(d_counter_, &h_cum_[size_t(G_) * tp.nb + 1], 8, cudaMemcpyHostToDevice, stream_),
                        "H2D unit counter");
+            h2d += (size_t(G_) * tp.nb + 2) * 8;
             tp.cum = d_cum_;
             tp.counter = d_counter_;
             if (tile_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
@@ -314,6 +321,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         check_cuda(cudaMemcpyAsync(h_state_.data(), pd_.state, h_state_.size(), cudaMemcpyDeviceToHost, stream_),
                    "D2H state");
         check_cuda(cudaStreamSynchronize(stream_), "level sync");
+        d2h += h_state_.size();
         float ms = 0;
         check_cuda(cudaEventElapsedTime(&ms, ev0_, ev1_), "event time");
         enum_s += ms * 1e-3;
@@ -362,6 +370,8 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     rep->best_generation = best_g;
     rep->best_gamma = best_j;
     rep->best_rank = best_r;
+    rep->h2d_bytes += h2d;
+    rep->d2h_bytes += d2h;
     if (best_out) {
         const BitMat &m = gammas_[size_t(std::max(0, best_j))].matrix;
         std::vector<uint64_t> acc(size_t(m.stride), 0);

@@ -49,6 +49,7 @@ class Plan {
              double *level_seconds);
 
     double h2d_seconds = 0;
+    unsigned long long upload_bytes = 0;
     int n_gammas() const { return G_; }
     int sentinel() const { return sentinel_; }
 
@@ -68,6 +69,7 @@ class Plan {
     std::vector<unsigned long long> h_binom_;
     int device_ = 0, num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
+    bool own_stream_ = true;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     void *d_mem_ = nullptr;
     ProblemDev pd_{};
