@@ -45,7 +45,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libsymdist_b200.so")
+# SDB_LIBRARY: alternate build of the same library (kernel-variant experiments only)
+_LIB_PATH = os.environ.get("SDB_LIBRARY") or os.path.join(HERE, "libsymdist_b200.so")
 
 # BASELINE.json configs: (n, k, seed); 3 is the 4096-code batch.
 CONFIGS = {

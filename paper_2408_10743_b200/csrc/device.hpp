@@ -2,9 +2,11 @@
 // singleton packages) and the kernel entry points in kernels.cu.
 //
 // HBM layout (one allocation per plan, all 16-byte aligned):
-//   rows  u32 [G][N][2W]   row r of Gamma_j: W x-words then W z-words (bit i of the
-//                          x-block = column i of the first half, i.e. the reference's
-//                          EnumMatrix symplectic split, engine.cpp:58-97)
+//   rows  u32 [G][N][2W]   row r of Gamma_j: W probe words then W partner words. Word w
+//                          of the pair holds symbols 32w..32w+31 of the x block or the z
+//                          block (the reference's EnumMatrix symplectic split,
+//                          engine.cpp:58-97); per (Gamma, w) the host puts the denser of the
+//                          two in the probe slot (orient_probe_words) — popc(x|z) is symmetric
 //   syn   u64 [G][N][SW]   compressed admissibility syndrome of each row (SW=0: no filter)
 //   binom u64 [N+1][BK]    saturating binomials C(a,b), b < BK
 //   state LevelState       per-level running minimum + per-weight best keys
@@ -12,6 +14,7 @@
 // route (Hamming weight of (a|b|a^b) = 2 popc(a|b), prep.hpp:66-68), 1 otherwise.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #ifdef __CUDACC__
@@ -71,9 +74,41 @@ int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, i
 // one XOR of two precomputed sums fused with the OR (2 LOP3) plus one POPC.
 constexpr int kTileThreads = 256;
 // heads held in registers per lane (2W words each); fewer for wide rows to avoid spills
-SDB_HD constexpr int heads_per_lane(int W) { return W <= 3 ? 8 : (W <= 5 ? 4 : 2); }
+#ifndef SDB_HEADS_W2
+#define SDB_HEADS_W2 8
+#endif
+SDB_HD constexpr int heads_per_lane(int W) { return W <= 2 ? SDB_HEADS_W2 : W <= 3 ? 8 : (W <= 5 ? 4 : 2); }
 SDB_HD constexpr int head_block(int W) { return kTileThreads * heads_per_lane(W); }
-constexpr int kTailChunk = 1024;
+#ifndef SDB_TAIL_CHUNK
+#define SDB_TAIL_CHUNK 1024
+#endif
+constexpr int kTailChunk = SDB_TAIL_CHUNK;
+// resident CTAs per SM (the register cap: 64 registers at 4, 80 at 3); measured on B200
+// (profiles/): W <= 2 runs best at 4, W = 3 spills there and runs best at 3
+#ifndef SDB_TILE_BLOCKS_W2
+#define SDB_TILE_BLOCKS_W2 4
+#endif
+#ifndef SDB_TILE_BLOCKS
+#define SDB_TILE_BLOCKS 3
+#endif
+SDB_HD constexpr int tile_blocks_per_sm(int W) { return W <= 2 ? SDB_TILE_BLOCKS_W2 : SDB_TILE_BLOCKS; }
+// Staged tail chunk: the probe words of each tail, [kTailChunk+1][probe_stride(W)] (W = 1
+// keeps both words of its single symbol block there: its fast path is exact). probe_stride
+// is even so two tails are whole 16-byte loads. The rare exact path rebuilds candidates
+// from the rows, so nothing else is staged per tail.
+SDB_HD constexpr int probe_stride(int W) { return W == 1 ? 2 : (W + 1) & ~1; }
+SDB_HD constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+struct TileSmem {
+    size_t rows, binom, tp, total;
+};
+SDB_HD inline TileSmem tile_smem_layout(int G, int N, int W, int BK) {
+    TileSmem L{};
+    L.rows = 0;
+    L.binom = align16(size_t(G) * N * 2 * W * 4);
+    L.tp = align16(L.binom + size_t(N + 1) * BK * 8);
+    L.total = align16(L.tp + size_t(kTailChunk + 1) * probe_stride(W) * 4);
+    return L;
+}
 
 struct TilePlan {
     int g, t, h;

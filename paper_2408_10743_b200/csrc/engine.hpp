@@ -83,6 +83,11 @@ class Plan {
 // the head x tail tile kernel. Exposed for tests.
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel);
 
+// Per Gamma and 32-symbol block, swap the x- and z-words of every row so that the word the
+// tile kernel's fast path folds (the first of the block) is the denser one. Weights are
+// unchanged (popc(x|z) is symmetric).
+void orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W);
+
 // Saturating binomial table (N+1) x BK.
 std::vector<unsigned long long> binom_table(int N, int BK);
 

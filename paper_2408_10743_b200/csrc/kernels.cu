@@ -238,76 +238,78 @@ __device__ __forceinline__ unsigned long long lexrank(const int *c, int g, int N
     return per - 1 - s;
 }
 
-// Rare path: a candidate whose exact weight passed the threshold. Rebuilds its element
-// list from the head rank and the tail rank, applies the admissibility syndrome and
-// publishes (weight, key). Returns the updated threshold.
-__device__ __noinline__ unsigned tile_publish(const ProblemDev p, const TilePlan tp, int j, int b,
-                                              unsigned long long head_rank, unsigned long long tail_rank,
-                                              const unsigned long long *tsyn, unsigned w, unsigned thrH) {
-    const int N = p.N, h = tp.h, t = tp.t;
+// Rare path: a candidate whose fast-path lower bound passed the threshold. Rebuilds its
+// element list from the head rank and the tail rank, computes the exact weight from the
+// rows, applies the admissibility syndrome (reference AdmissibilityFilter,
+// engine.cpp:14-29) and publishes (weight, key). Returns the updated threshold.
+template <int W>
+__device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan tp, const uint32_t *grows, int j, int b,
+                                            unsigned long long head_rank, unsigned long long tail_rank,
+                                            unsigned thrH) {
+    const int N = p.N, h = tp.h, t = tp.t, g = tp.g;
     int c[kMaxLevel];
     unrank_colex(head_rank, h, b, p.binom, p.BK, c);
     c[h] = b;
     unrank_colex(tail_rank, t - 1, N - 1 - b, p.binom, p.BK, c + h + 1);
-    for (int k = h + 1; k < h + t; k++) c[k] += b + 1;
+    for (int k = h + 1; k < g; k++) c[k] += b + 1;
+    uint32_t acc[2 * W];
+#pragma unroll
+    for (int w = 0; w < 2 * W; w++) acc[w] = 0;
+    for (int k = 0; k < g; k++) xor_row<W>(acc, grows + c[k] * 2 * W);
+    const unsigned wv = unsigned(p.scale * weight_of<W>(acc));
+    if (wv > thrH) return thrH;
     if (p.SW) {
         const unsigned long long *syn = p.syn + (size_t)j * N * p.SW;
         bool adm = false;
         for (int s = 0; s < p.SW; s++) {
-            unsigned long long x = tsyn[s];
-            for (int k = 0; k < h; k++) x ^= syn[c[k] * p.SW + s];
+            unsigned long long x = 0;
+            for (int k = 0; k < g; k++) x ^= syn[c[k] * p.SW + s];
             adm |= x != 0;
         }
         if (!adm) return thrH;
     }
     const unsigned long long key =
-        ((unsigned long long)j << kKeyRankBits) | lexrank(c, tp.g, N, p.binom, p.BK, tp.per_gamma);
-    atomicMin(&p.state->wmin, w);
-    atomicMin(&p.key_by_w[w], key);
-    return w;
+        ((unsigned long long)j << kKeyRankBits) | lexrank(c, g, N, p.binom, p.BK, tp.per_gamma);
+    atomicMin(&p.state->wmin, wv);
+    atomicMin(&p.key_by_w[wv], key);
+    return wv;
 }
 
-// OR-fold of the W words of (x ^ tx) | (z ^ tz): popc of the fold is a lower bound on the
-// candidate's weight (exact for W = 1), one POPC per candidate whatever W is.
+// Fast-path lower bound on a candidate's weight (in symbols), one POPC whatever W is:
+// the OR over the W blocks of the probe-word differences. Bit b of the fold is set only if
+// some symbol 32w+b of the candidate is nonzero, so popc(fold) <= popc(x|z). W = 1 folds
+// both words of its single block and is exact.
 template <int W>
-__device__ __forceinline__ uint32_t fold(const uint32_t (&hx)[W], const uint32_t (&hz)[W], const uint32_t *t) {
-    uint32_t u = (hx[0] ^ t[0]) | (hz[0] ^ t[W]);
+__device__ __forceinline__ uint32_t probe_fold(const uint32_t (&hp)[W], const uint32_t (&hq)[W], const uint32_t *t) {
+    if constexpr (W == 1) {
+        return (hp[0] ^ t[0]) | (hq[0] ^ t[1]);
+    } else {
+        uint32_t u = hp[0] ^ t[0];
 #pragma unroll
-    for (int w = 1; w < W; w++) u |= (hx[w] ^ t[w]) | (hz[w] ^ t[W + w]);
-    return u;
+        for (int w = 1; w < W; w++) u |= hp[w] ^ t[w];
+        return u;
+    }
 }
 
 template <int W>
-__device__ __forceinline__ unsigned exact_weight(const uint32_t (&hx)[W], const uint32_t (&hz)[W], const uint32_t *t) {
-    unsigned s = 0;
-#pragma unroll
-    for (int w = 0; w < W; w++) s += __popc((hx[w] ^ t[w]) | (hz[w] ^ t[W + w]));
-    return s;
-}
-
-template <int W>
-__global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, TilePlan tp) {
+__global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kernel(ProblemDev p, TilePlan tp) {
     constexpr int H = heads_per_lane(W);
     constexpr int HB = head_block(W);
+    constexpr int PW = probe_stride(W);
+    constexpr int HQ = W == 1 ? H : 1;  // partner words are only needed in registers when W = 1
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowlen = 2 * W;
-    const int G = p.G, N = p.N, SW = p.SW;
+    const int G = p.G, N = p.N;
+    const TileSmem lay = tile_smem_layout(G, N, W, p.BK);
     const int nrow_words = G * N * rowlen;
-    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem);
-    unsigned long long *s_binom =
-        reinterpret_cast<unsigned long long *>(smem + ((nrow_words * 4 + 15) & ~15));
+    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem + lay.rows);
+    unsigned long long *s_binom = reinterpret_cast<unsigned long long *>(smem + lay.binom);
     const int nbinom = (N + 1) * p.BK;
-    unsigned long long *s_syn = s_binom + nbinom;
-    const int nsyn = G * N * SW;
-    // tail chunk: 2W words per tail (x block then z block), one spare tail for odd counts
-    uint32_t *s_tail = reinterpret_cast<uint32_t *>(s_syn + nsyn + (nsyn & 1));
-    unsigned long long *s_tsyn =
-        reinterpret_cast<unsigned long long *>(s_tail + (((kTailChunk + 1) * rowlen + 3) & ~3));
+    uint32_t *s_tp = reinterpret_cast<uint32_t *>(smem + lay.tp);
     __shared__ unsigned long long s_unit;
     __shared__ unsigned long long s_visited;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[i];
-    for (int i = threadIdx.x; i < nsyn; i += blockDim.x) s_syn[i] = p.syn[i];
     if (threadIdx.x == 0) s_visited = 0;
 
     const int t = tp.t, h = tp.h;
@@ -335,26 +337,23 @@ __global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, Til
         const unsigned long long t0 = tc * kTailChunk;
         const int tcount = int(min((unsigned long long)kTailChunk, Tb - t0));
         const uint32_t *grows = s_rows + j * N * rowlen;
-        const unsigned long long *gsyn = s_syn + j * N * SW;
 
-        // stage the tail chunk: {b} + colex (t-1)-subsets of (b, N)
+        // stage the tail chunk's probe words: {b} + colex (t-1)-subsets of (b, N)
         for (int i = threadIdx.x; i < tcount; i += blockDim.x) {
             int e[kMaxLevel];
             unrank_colex(t0 + i, t - 1, N - 1 - b, s_binom, p.BK, e);
-            uint32_t acc[2 * W];
+            constexpr int SW_ = W == 1 ? 2 : W;  // words staged per tail
+            uint32_t acc[SW_];
 #pragma unroll
-            for (int w = 0; w < 2 * W; w++) acc[w] = grows[b * rowlen + w];
-            for (int k = 0; k < t - 1; k++) xor_row<W>(acc, grows + (b + 1 + e[k]) * rowlen);
-            for (int s = 0; s < SW; s++) {
-                unsigned long long x = gsyn[b * SW + s];
-                for (int k = 0; k < t - 1; k++) x ^= gsyn[(b + 1 + e[k]) * SW + s];
-                s_tsyn[i * SW + s] = x;
-            }
+            for (int w = 0; w < SW_; w++) acc[w] = grows[b * rowlen + w];
+            for (int k = 0; k < t - 1; k++)
 #pragma unroll
-            for (int w = 0; w < 2 * W; w++) s_tail[i * rowlen + w] = acc[w];
-            if (i == tcount - 1 && (tcount & 1))  // pad odd counts with a duplicate
+                for (int w = 0; w < SW_; w++) acc[w] ^= grows[(b + 1 + e[k]) * rowlen + w];
+            // odd counts: pad with a duplicate of the last tail (same candidates)
+            const int copies = (i == tcount - 1 && (tcount & 1)) ? 2 : 1;
+            for (int r = 0; r < copies; r++)
 #pragma unroll
-                for (int w = 0; w < 2 * W; w++) s_tail[(i + 1) * rowlen + w] = acc[w];
+                for (int w = 0; w < SW_; w++) s_tp[(i + r) * PW + w] = acc[w];
         }
         __syncthreads();
 
@@ -366,7 +365,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, Til
             s_visited += blk * (unsigned long long)tcount;
         }
         if (!__any_sync(0xffffffffu, nvalid > 0)) continue;
-        uint32_t hx[H][W], hz[H][W];
+        uint32_t hp[H][W], hq[HQ][W];
         {
             int e[kMaxLevel];
             uint32_t x[W], z[W];
@@ -381,7 +380,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, Til
                         z[w] ^= grows[e[k] * rowlen + W + w];
                     }
             } else {
-                // lanes without heads: all-ones fold, never passes the threshold check below
+                // lanes without heads: all-ones probe words, the fold never passes the check
 #pragma unroll
                 for (int w = 0; w < W; w++) x[w] = z[w] = 0xffffffffu;
             }
@@ -395,7 +394,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, Til
 #pragma unroll
                         for (int w = 0; w < W; w++) {
                             x[w] ^= grows[e[k] * rowlen + w];
-                            z[w] ^= grows[e[k] * rowlen + W + w];
+                            if (W == 1) z[w] ^= grows[e[k] * rowlen + W + w];
                         }
                     e[q]++;
                     for (int k = 0; k < q; k++) e[k] = k;
@@ -403,43 +402,48 @@ __global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, Til
 #pragma unroll
                         for (int w = 0; w < W; w++) {
                             x[w] ^= grows[e[k] * rowlen + w];
-                            z[w] ^= grows[e[k] * rowlen + W + w];
+                            if (W == 1) z[w] ^= grows[e[k] * rowlen + W + w];
                         }
                 }
                 // heads past the valid count repeat the last valid head (same candidates)
 #pragma unroll
                 for (int w = 0; w < W; w++) {
-                    hx[i][w] = x[w];
-                    hz[i][w] = z[w];
+                    hp[i][w] = x[w];
+                    if (W == 1) hq[W == 1 ? i : 0][w] = z[w];
                 }
             }
         }
 
         unsigned thr0 = thrH >> sshift;
         for (int ti = 0; ti < tcount; ti += 2) {
-            const uint32_t *ta = s_tail + ti * rowlen;
-            const uint32_t *tb = ta + rowlen;
+            // both tails' probe words: 2 * PW words, whole 16-byte broadcast loads
+            uint32_t tt[2 * PW];
+#pragma unroll
+            for (int v = 0; v < 2 * PW; v += 4) {
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(s_tp + ti * PW + v);
+                tt[v] = q4.x;
+                tt[v + 1] = q4.y;
+                tt[v + 2] = q4.z;
+                tt[v + 3] = q4.w;
+            }
             unsigned m = 0xffffffffu;
 #pragma unroll
             for (int i = 0; i < H; i++) {
-                const unsigned a = __popc(fold<W>(hx[i], hz[i], ta));
-                const unsigned c = __popc(fold<W>(hx[i], hz[i], tb));
+                const unsigned a = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt));
+                const unsigned c = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt + PW));
                 m = min(m, min(a, c));
             }
             if (m <= thr0 && nvalid > 0) {
-                // rare: exact weights for this tail pair
+                // rare: candidates of this tail pair whose bound passed, exact from the rows
+#pragma unroll 1
+                for (int r = 0; r < 2; r++) {
+                    const int tix = ti + r;
+                    if (tix >= tcount) break;
 #pragma unroll
-                for (int i = 0; i < H; i++) {
-                    if (i < nvalid) {
-                        const unsigned wa = exact_weight<W>(hx[i], hz[i], ta) << sshift;
-                        if (wa <= thrH) {
-                            thrH = tile_publish(p, tp, j, b, hbase + i, t0 + ti, s_tsyn + ti * SW, wa, thrH);
-                            thr0 = thrH >> sshift;
-                        }
-                        const unsigned wb = exact_weight<W>(hx[i], hz[i], tb) << sshift;
-                        if (ti + 1 < tcount && wb <= thrH) {
-                            thrH = tile_publish(p, tp, j, b, hbase + i, t0 + ti + 1, s_tsyn + (ti + 1) * SW, wb,
-                                                thrH);
+                    for (int i = 0; i < H; i++) {
+                        if (i < nvalid &&
+                            __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], s_tp + tix * PW)) <= thr0) {
+                            thrH = tile_exact<W>(p, tp, grows, j, b, hbase + i, t0 + tix, thrH);
                             thr0 = thrH >> sshift;
                         }
                     }
@@ -451,13 +455,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) tile_kernel(ProblemDev p, Til
     if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
 }
 
-size_t tile_smem(int G, int N, int W, int SW, int BK) {
-    size_t base = ((size_t(G) * N * 2 * W * 4 + 15) & ~size_t(15)) + size_t(N + 1) * BK * 8 + size_t(G) * N * SW * 8;
-    base += (size_t(G) * N * SW & 1) * 8;
-    base += size_t(((kTailChunk + 1) * 2 * W + 3) & ~3) * 4;
-    base += size_t(kTailChunk) * SW * 8;
-    return base;
-}
+size_t tile_smem(int G, int N, int W, int SW, int BK) { (void)SW; return tile_smem_layout(G, N, W, BK).total; }
 
 template <int W>
 int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, int num_sms) {
