@@ -39,12 +39,27 @@ struct LevelState {
     // followed in memory by key_by_w[max_weight + 1] (u64)
 };
 
+// Device-resident level-loop state (reference BoundsState, engine.hpp:26-33): the host
+// enqueues levels without waiting for each one; level_close folds a level's minimum into
+// U, writes the trace entry and raises `done` once L(g) >= U, after which every later
+// level kernel returns at once.
+struct RunCtl {
+    unsigned int U;                 // upper bound in engine units
+    int done;                       // 1 once L(g) >= U (reference run_bz break, engine.cpp:334)
+    int best_g;                     // level of the best candidate (-1: none)
+    int pad;
+    unsigned long long best_key;    // gamma << 58 | lexicographic rank
+    unsigned long long visited;     // candidates the kernels enumerated, all levels
+};
+
 struct ProblemDev {
     const uint32_t *rows;
     const unsigned long long *syn;
     const unsigned long long *binom;
     LevelState *state;
     unsigned long long *key_by_w;
+    RunCtl *ctl;
+    int *trace_upper;               // [N + 1]: U after level g (-1: level skipped)
     int G, N, W, SW, BK;
     int scale;
     int max_weight;
@@ -58,6 +73,12 @@ struct LevelLaunch {
     unsigned long long segs_per_gamma;
     unsigned long long seg_begin, seg_end;  // this rank's shard of [0, G * segs_per_gamma)
 };
+
+// Level-loop control kernels (one CTA each): reset U / best / counters for a run, and
+// close one level (fold the level minimum into U, trace, termination, reset the level).
+int launch_run_init(const ProblemDev &p, unsigned sentinel, const unsigned long long *counter_init,
+                    unsigned long long *counters, int n_counters, void *stream);
+int launch_level_close(const ProblemDev &p, int g, long long lower, void *stream);
 
 // One level, all matrices, lexicographic-walk kernel. Returns the number of kernels launched.
 int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, int num_sms);

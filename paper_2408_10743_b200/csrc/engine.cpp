@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <thread>
 
 #include "errors.hpp"
@@ -179,11 +180,86 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
     upload();
 }
 
+// ---- process-wide caches: repeated distance calls skip cudaMalloc / stream / event creation
+namespace {
+std::mutex g_cache_mu;
+struct FreeBlock {
+    int device;
+    size_t bytes;
+    void *ptr;
+};
+std::vector<FreeBlock> g_free_blocks;
+std::vector<std::pair<int, cudaEvent_t>> g_free_events;
+
+void *workspace_get(int device, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        size_t best = g_free_blocks.size();
+        for (size_t i = 0; i < g_free_blocks.size(); i++) {
+            const FreeBlock &f = g_free_blocks[i];
+            if (f.device == device && f.bytes >= bytes && f.bytes <= 4 * bytes + (1 << 20) &&
+                (best == g_free_blocks.size() || f.bytes < g_free_blocks[best].bytes))
+                best = i;
+        }
+        if (best < g_free_blocks.size()) {
+            void *p = g_free_blocks[best].ptr;
+            g_free_blocks.erase(g_free_blocks.begin() + long(best));
+            return p;
+        }
+    }
+    void *p = nullptr;
+    check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+    return p;
+}
+
+void workspace_put(int device, size_t bytes, void *p) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_free_blocks.push_back(FreeBlock{device, bytes, p});
+    if (g_free_blocks.size() > 16) {
+        cudaFree(g_free_blocks.front().ptr);
+        g_free_blocks.erase(g_free_blocks.begin());
+    }
+}
+
+cudaEvent_t event_get(int device) {
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_free_events.size(); i++)
+            if (g_free_events[i].first == device) {
+                cudaEvent_t e = g_free_events[i].second;
+                g_free_events.erase(g_free_events.begin() + long(i));
+                return e;
+            }
+    }
+    cudaEvent_t e;
+    check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void event_put(int device, cudaEvent_t e) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_free_events.emplace_back(device, e);
+}
+
+// one non-blocking stream per (thread, device), kept for the process lifetime
+cudaStream_t thread_stream(int device) {
+    thread_local std::vector<std::pair<int, cudaStream_t>> streams;
+    for (auto &s : streams)
+        if (s.first == device) return s.second;
+    cudaStream_t st;
+    check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    streams.emplace_back(device, st);
+    return st;
+}
+}  // namespace
+
 Plan::~Plan() {
-    if (d_mem_) cudaFree(d_mem_);
-    if (ev0_) cudaEventDestroy(ev0_);
-    if (ev1_) cudaEventDestroy(ev1_);
-    if (stream_ && own_stream_) cudaStreamDestroy(stream_);
+    if (d_mem_) {
+        cudaStreamSynchronize(stream_);
+        workspace_put(device_, d_bytes_, d_mem_);
+    }
+    for (cudaEvent_t e : events_)
+        if (e) event_put(device_, e);
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -192,20 +268,17 @@ void Plan::upload() {
     device_ = opts_.device;
     check_cuda(cudaSetDevice(device_), "cudaSetDevice");
     check_cuda(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_), "cudaDeviceGetAttribute");
-    if (opts_.stream) {
-        stream_ = static_cast<cudaStream_t>(opts_.stream);
-        own_stream_ = false;
-    } else {
-        check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
-    }
-    check_cuda(cudaEventCreate(&ev0_), "cudaEventCreate");
-    check_cuda(cudaEventCreate(&ev1_), "cudaEventCreate");
+    stream_ = opts_.stream ? static_cast<cudaStream_t>(opts_.stream) : thread_stream(device_);
+    // tile unit tables: level g needs G * (N - g + 1) + 1 entries (boundaries b in [h, N - t])
+    table_cap_ = size_t(G_) * size_t(N_ + 1) * size_t(N_ + 2) / 2 + size_t(N_ + 2);
     const size_t b_rows = align256(h_rows_.size() * 4), b_syn = align256(std::max<size_t>(h_syn_.size(), 1) * 8),
                  b_binom = align256(h_binom_.size() * 8),
-                 b_state = align256(sizeof(LevelState) + size_t(max_weight_ + 1) * 8);
-    const size_t b_cum = align256((size_t(G_) * (N_ + 1) + 2) * 8);
+                 b_state = align256(sizeof(LevelState) + size_t(max_weight_ + 1) * 8),
+                 b_ctl = align256(sizeof(RunCtl)), b_trace = align256(size_t(N_ + 1) * 4),
+                 b_counters = align256(size_t(N_ + 1) * 8), b_tables = align256(table_cap_ * 8);
+    d_bytes_ = b_rows + b_syn + b_binom + b_state + b_ctl + b_trace + 2 * b_counters + b_tables;
     const auto t0 = std::chrono::steady_clock::now();
-    check_cuda(cudaMalloc(&d_mem_, b_rows + b_syn + b_binom + b_state + b_cum), "cudaMalloc");
+    d_mem_ = workspace_get(device_, d_bytes_);
     unsigned char *base = static_cast<unsigned char *>(d_mem_);
     check_cuda(cudaMemcpyAsync(base, h_rows_.data(), h_rows_.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D rows");
     if (!h_syn_.empty())
@@ -214,17 +287,29 @@ void Plan::upload() {
     check_cuda(cudaMemcpyAsync(base + b_rows + b_syn, h_binom_.data(), h_binom_.size() * 8, cudaMemcpyHostToDevice,
                                stream_),
                "H2D binom");
-    check_cuda(cudaStreamSynchronize(stream_), "H2D sync");
-    h2d_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     upload_bytes = h_rows_.size() * 4 + h_syn_.size() * 8 + h_binom_.size() * 8;
+    unsigned char *q = base + b_rows + b_syn + b_binom;
     pd_.rows = reinterpret_cast<const uint32_t *>(base);
     pd_.syn = reinterpret_cast<const unsigned long long *>(base + b_rows);
     pd_.binom = reinterpret_cast<const unsigned long long *>(base + b_rows + b_syn);
-    pd_.state = reinterpret_cast<LevelState *>(base + b_rows + b_syn + b_binom);
-    pd_.key_by_w = reinterpret_cast<unsigned long long *>(base + b_rows + b_syn + b_binom + sizeof(LevelState));
-    d_cum_ = reinterpret_cast<unsigned long long *>(base + b_rows + b_syn + b_binom + b_state);
-    d_counter_ = d_cum_ + size_t(G_) * (N_ + 1) + 1;
-    h_cum_.assign(size_t(G_) * (N_ + 1) + 2, 0);
+    pd_.state = reinterpret_cast<LevelState *>(q);
+    pd_.key_by_w = reinterpret_cast<unsigned long long *>(q + sizeof(LevelState));
+    q += b_state;
+    pd_.ctl = reinterpret_cast<RunCtl *>(q);
+    q += b_ctl;
+    pd_.trace_upper = reinterpret_cast<int *>(q);
+    q += b_trace;
+    d_counters_ = reinterpret_cast<unsigned long long *>(q);
+    q += b_counters;
+    d_counter_init_ = reinterpret_cast<unsigned long long *>(q);
+    q += b_counters;
+    d_tables_ = reinterpret_cast<unsigned long long *>(q);
+    h_counter_init_.assign(size_t(N_ + 1), 0);
+    check_cuda(cudaMemcpyAsync(d_counter_init_, h_counter_init_.data(), size_t(N_ + 1) * 8, cudaMemcpyHostToDevice,
+                               stream_),
+               "H2D counters");
+    check_cuda(cudaStreamSynchronize(stream_), "H2D sync");
+    h2d_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     pd_.G = G_;
     pd_.N = N_;
     pd_.W = W_;
@@ -232,9 +317,15 @@ void Plan::upload() {
     pd_.BK = BK_;
     pd_.scale = scale_;
     pd_.max_weight = max_weight_;
-    h_state_.assign(sizeof(LevelState) + size_t(max_weight_ + 1) * 8, 0);
+    levels_.assign(size_t(N_ + 1), LevelHost{});
+    events_.assign(size_t(2 * (N_ + 1)), nullptr);
     if (problem_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
         throw InvalidArgument("problem too large for shared-memory staging");
+}
+
+cudaEvent_t Plan::level_event(int i) {
+    if (!events_[size_t(i)]) events_[size_t(i)] = event_get(device_);
+    return events_[size_t(i)];
 }
 
 size_t tile_smem_bytes(int G, int N, int W, int SW, int BK);
@@ -282,110 +373,157 @@ long long Plan::lower_bound(int g) const {
     throw InvalidArgument("lower_bound: symplectic mode takes one or two matrices");
 }
 
-void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out, double *level_seconds) {
-    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+void Plan::prepare_level(int g) {
+    LevelHost &lv = levels_[size_t(g)];
+    if (lv.ready) return;
     const int world = std::max(1, opts_.world), rank = opts_.rank;
-    if (rank < 0 || rank >= world) throw InvalidArgument("rank outside [0, world)");
-    if (world > 1 && !opts_.allreduce_min) throw InvalidArgument("world > 1 needs an allreduce_min callback");
-    long long U = sentinel_, L = 1;
-    int generation = 0, launches = 0;
-    unsigned long long candidates = 0, visited = 0, h2d = 0, d2h = 0;
-    double enum_s = 0;
-    int best_g = -1, best_j = -1;
-    unsigned long long best_r = 0;
-    int g_limit = N_;
-    if (opts_.max_generation > 0) g_limit = std::min(g_limit, opts_.max_generation);
-    bool complete = false;
-    int n_levels = 0;
-    const int threads_total = num_sms_ * 8 * 256;
-    for (int g = 1; g <= g_limit; g++) {
-        if (g > kMaxLevel) throw InvalidArgument("generation beyond the kernels' combination-size limit");
-        const unsigned long long per = binom_u64(N_, g);
-        if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
-        LevelLaunch LL{};
+    const unsigned long long per = binom_u64(N_, g);
+    if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
+    const unsigned long long total = per * (unsigned long long)G_;
+    lv.t = choose_tile_t(G_, N_, g, W_, per, opts_.kernel);
+    if (lv.t == 0) {
+        LevelLaunch &LL = lv.walk;
         LL.g = g;
-        LL.thr0 = unsigned(U - 1);
+        LL.thr0 = ~0u;  // the kernels read U from the device (RunCtl)
         LL.per_gamma = per;
-        const unsigned long long total = per * (unsigned long long)G_;
-        unsigned long long seg = (total + (unsigned long long)threads_total * 4 - 1) / ((unsigned long long)threads_total * 4);
+        const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
+        const unsigned long long seg = (total + threads_total * 4 - 1) / (threads_total * 4);
         LL.seg_len = std::max<unsigned long long>(64, seg);
         LL.segs_per_gamma = (per + LL.seg_len - 1) / LL.seg_len;
         const unsigned long long S = LL.segs_per_gamma * (unsigned long long)G_;
         LL.seg_begin = (unsigned long long)((unsigned __int128)S * rank / world);
         LL.seg_end = (unsigned long long)((unsigned __int128)S * (rank + 1) / world);
-        check_cuda(cudaMemsetAsync(pd_.state, 0xFF, h_state_.size(), stream_), "memset state");
-        check_cuda(cudaMemsetAsync(&pd_.state->visited, 0, 8, stream_), "memset visited");
-        check_cuda(cudaEventRecord(ev0_, stream_), "event");
-        const int t = choose_tile_t(G_, N_, g, W_, per, opts_.kernel);
-        int nl;
-        if (t == 0) {
-            nl = launch_walk_level(pd_, LL, stream_, num_sms_);
-        } else {
-            TilePlan tp{};
-            tp.g = g;
-            tp.t = t;
-            tp.h = g - t;
-            tp.thr0 = unsigned(U - 1);
-            tp.nb = N_ - t - tp.h + 1;
-            tp.per_gamma = per;
-            unsigned long long acc = 0;
-            for (int j = 0; j < G_; j++)
-                for (int b = tp.h; b <= N_ - t; b++) {
-                    h_cum_[size_t(j) * tp.nb + (b - tp.h)] = acc;
-                    const unsigned long long Hb = binom_u64(b, tp.h), Tb = binom_u64(N_ - 1 - b, t - 1);
-                    acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + kTailChunk - 1) / kTailChunk);
-                }
-            h_cum_[size_t(G_) * tp.nb] = acc;
-            tp.unit_begin = (unsigned long long)((unsigned __int128)acc * rank / world);
-            tp.unit_end = (unsigned long long)((unsigned __int128)acc * (rank + 1) / world);
-            h_cum_[size_t(G_) * tp.nb + 1] = tp.unit_begin;  // staged counter start
-            check_cuda(cudaMemcpyAsync(d_cum_, h_cum_.data(), (size_t(G_) * tp.nb + 1) * 8, cudaMemcpyHostToDevice,
-                                       stream_),
-                       "H2D unit table");
-            check_cuda(cudaMemcpyAsync(d_counter_, &h_cum_[size_t(G_) * tp.nb + 1], 8, cudaMemcpyHostToDevice, stream_),
-                       "H2D unit counter");
-            h2d += (size_t(G_) * tp.nb + 2) * 8;
-            tp.cum = d_cum_;
-            tp.counter = d_counter_;
-            if (tile_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
-                throw InvalidArgument("problem too large for shared-memory staging");
-            nl = launch_tile_level(pd_, tp, stream_, num_sms_);
-        }
+    } else {
+        TilePlan &tp = lv.tile;
+        tp.g = g;
+        tp.t = lv.t;
+        tp.h = g - lv.t;
+        tp.thr0 = ~0u;
+        tp.nb = N_ - lv.t - tp.h + 1;
+        tp.per_gamma = per;
+        const size_t n_entries = size_t(G_) * size_t(tp.nb) + 1;
+        if (table_used_ + n_entries > table_cap_) throw InternalFailure("tile unit tables overflow");
+        h_table_.resize(n_entries);
+        unsigned long long acc = 0;
+        for (int j = 0; j < G_; j++)
+            for (int b = tp.h; b <= N_ - lv.t; b++) {
+                h_table_[size_t(j) * tp.nb + (b - tp.h)] = acc;
+                const unsigned long long Hb = binom_u64(b, tp.h), Tb = binom_u64(N_ - 1 - b, lv.t - 1);
+                acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + kTailChunk - 1) / kTailChunk);
+            }
+        h_table_[size_t(G_) * tp.nb] = acc;
+        tp.unit_begin = (unsigned long long)((unsigned __int128)acc * rank / world);
+        tp.unit_end = (unsigned long long)((unsigned __int128)acc * (rank + 1) / world);
+        tp.cum = d_tables_ + table_used_;
+        tp.counter = d_counters_ + g;
+        table_used_ += n_entries;
+        h_counter_init_[size_t(g)] = tp.unit_begin;
+        // pageable sources: the copies are staged before cudaMemcpyAsync returns
+        check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table_.data(), n_entries * 8,
+                                   cudaMemcpyHostToDevice, stream_),
+                   "H2D unit table");
+        check_cuda(cudaMemcpyAsync(d_counter_init_ + g, &h_counter_init_[size_t(g)], 8, cudaMemcpyHostToDevice, stream_),
+                   "H2D unit counter");
+        check_cuda(cudaMemcpyAsync(d_counters_ + g, &h_counter_init_[size_t(g)], 8, cudaMemcpyHostToDevice, stream_),
+                   "H2D unit counter");
+        check_cuda(cudaStreamSynchronize(stream_), "H2D unit table sync");
+        if (tile_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
+            throw InvalidArgument("problem too large for shared-memory staging");
+    }
+    lv.ready = true;
+}
+
+// The level loop (reference run_bz, engine.cpp:303-343) with the bound state on the device:
+// levels are enqueued without waiting; level_close folds each level into U, writes the
+// trace entry and raises `done` once L(g) >= U, and every later kernel returns at once.
+// The host waits only after levels big enough to matter (and, with several ranks, after
+// every level for the min-allreduce of the level minimum).
+void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out, double *level_seconds) {
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    const int world = std::max(1, opts_.world), rank = opts_.rank;
+    if (rank < 0 || rank >= world) throw InvalidArgument("rank outside [0, world)");
+    if (world > 1 && !opts_.allreduce_min) throw InvalidArgument("world > 1 needs an allreduce_min callback");
+    int g_limit = N_;
+    if (opts_.max_generation > 0) g_limit = std::min(g_limit, opts_.max_generation);
+    if (g_limit > kMaxLevel) g_limit = kMaxLevel;  // checked again below if the run gets there
+    constexpr unsigned long long kSyncCandidates = 1ull << 28;  // ~0.1 ms of kernel time
+    int launches = 0, last_g = 0;
+    unsigned long long h2d = 0, d2h = 0;
+    launches += launch_run_init(pd_, unsigned(sentinel_), d_counter_init_, d_counters_, N_ + 1, stream_);
+    check_cuda(cudaGetLastError(), "run init launch");
+    RunCtl ctl{};
+    std::vector<unsigned char> h_state;
+    for (int g = 1; g <= g_limit; g++) {
+        prepare_level(g);
+        const LevelHost &lv = levels_[size_t(g)];
+        check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
+        const int nl = lv.t == 0 ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
+                                 : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
         if (nl < 0) throw InvalidArgument("unsupported row width");
         launches += nl;
-        check_cuda(cudaGetLastError(), "walk kernel launch");
-        check_cuda(cudaEventRecord(ev1_, stream_), "event");
-        check_cuda(cudaMemcpyAsync(h_state_.data(), pd_.state, h_state_.size(), cudaMemcpyDeviceToHost, stream_),
-                   "D2H state");
-        check_cuda(cudaStreamSynchronize(stream_), "level sync");
-        d2h += h_state_.size();
-        float ms = 0;
-        check_cuda(cudaEventElapsedTime(&ms, ev0_, ev1_), "event time");
-        enum_s += ms * 1e-3;
-        LevelState st;
-        std::memcpy(&st, h_state_.data(), sizeof st);
-        const unsigned long long *keys = reinterpret_cast<const unsigned long long *>(h_state_.data() + sizeof st);
-        uint64_t wmin = st.wmin == ~0u ? ~uint64_t(0) : uint64_t(st.wmin);
-        uint64_t key = wmin != ~uint64_t(0) ? keys[wmin] : kNoKey;
-        visited += st.visited;
+        check_cuda(cudaGetLastError(), "level kernel launch");
         if (world > 1) {
+            // min-allreduce of (level minimum, its key) across ranks, then hand the result
+            // to level_close through the same state fields
+            const size_t sb = sizeof(LevelState) + size_t(max_weight_ + 1) * 8;
+            h_state.resize(sb);
+            check_cuda(cudaMemcpyAsync(h_state.data(), pd_.state, sb, cudaMemcpyDeviceToHost, stream_), "D2H state");
+            check_cuda(cudaStreamSynchronize(stream_), "level sync");
+            d2h += sb;
+            LevelState st;
+            std::memcpy(&st, h_state.data(), sizeof st);
+            const unsigned long long *keys = reinterpret_cast<const unsigned long long *>(h_state.data() + sizeof st);
+            uint64_t wmin = st.wmin == ~0u ? ~uint64_t(0) : uint64_t(st.wmin);
+            uint64_t key = wmin != ~uint64_t(0) ? keys[wmin] : kNoKey;
             uint64_t v = wmin;
             if (opts_.allreduce_min(opts_.allreduce_ctx, &v, 1) != 0) throw DeviceFailure("allreduce_min failed");
             if (v != wmin) key = kNoKey;
-            wmin = v;
-            uint64_t k2 = key;
-            if (opts_.allreduce_min(opts_.allreduce_ctx, &k2, 1) != 0) throw DeviceFailure("allreduce_min failed");
-            key = k2;
+            if (opts_.allreduce_min(opts_.allreduce_ctx, &key, 1) != 0) throw DeviceFailure("allreduce_min failed");
+            static thread_local unsigned hw[2];
+            static thread_local unsigned long long hk;
+            hw[0] = v == ~uint64_t(0) ? ~0u : unsigned(v);
+            hk = key;
+            check_cuda(cudaMemcpyAsync(&pd_.state->wmin, &hw[0], 4, cudaMemcpyHostToDevice, stream_), "H2D wmin");
+            h2d += 4;
+            if (v != ~uint64_t(0)) {
+                check_cuda(cudaMemcpyAsync(pd_.key_by_w + v, &hk, 8, cudaMemcpyHostToDevice, stream_), "H2D key");
+                h2d += 8;
+            }
         }
-        if (wmin != ~uint64_t(0) && (long long)wmin < U) {
-            U = (long long)wmin;
-            best_g = g;
-            best_j = int(key >> kKeyRankBits);
-            best_r = key & ((1ull << kKeyRankBits) - 1);
+        launches += launch_level_close(pd_, g, lower_bound(g), stream_);
+        check_cuda(cudaGetLastError(), "level close launch");
+        check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
+        last_g = g;
+        const unsigned long long total = binom_u64(N_, g) * (unsigned long long)G_;
+        if (world > 1 || total >= kSyncCandidates || g == g_limit) {
+            check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
+            check_cuda(cudaStreamSynchronize(stream_), "level sync");
+            d2h += sizeof ctl;
+            if (ctl.done) break;
         }
-        candidates += total;
+        if (g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
+            throw InvalidArgument("generation beyond the kernels' combination-size limit");
+    }
+    std::vector<int> tu(size_t(last_g + 1));
+    check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
+    check_cuda(cudaMemcpyAsync(tu.data(), pd_.trace_upper, tu.size() * 4, cudaMemcpyDeviceToHost, stream_), "D2H trace");
+    check_cuda(cudaStreamSynchronize(stream_), "run sync");
+    d2h += sizeof ctl + tu.size() * 4;
+
+    long long U = sentinel_;
+    unsigned long long candidates = 0;
+    double enum_s = 0;
+    int generation = 0, n_levels = 0;
+    bool complete = false;
+    for (int g = 1; g <= last_g; g++) {
+        if (tu[size_t(g)] < 0) break;  // enqueued after termination: skipped on the device
+        U = tu[size_t(g)];
+        const long long L = lower_bound(g);
+        float ms = 0;
+        check_cuda(cudaEventElapsedTime(&ms, level_event(2 * g), level_event(2 * g + 1)), "event time");
+        enum_s += ms * 1e-3;
+        candidates += binom_u64(N_, g) * (unsigned long long)G_;
         generation = g;
-        L = lower_bound(g);
         if (n_levels < trace_cap && trace) trace[n_levels] = sdb_trace_entry{g, L, U};
         if (level_seconds && n_levels < trace_cap) level_seconds[n_levels] = ms * 1e-3;
         n_levels++;
@@ -395,12 +533,15 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     if (complete && U >= sentinel_)
         throw InternalFailure("run_bz: no admissible codeword after complete enumeration; "
                               "input is not a valid normalizer matrix");
+    const int best_g = ctl.best_g;
+    const int best_j = best_g > 0 ? int(ctl.best_key >> kKeyRankBits) : -1;
+    const unsigned long long best_r = best_g > 0 ? (ctl.best_key & ((1ull << kKeyRankBits) - 1)) : 0;
     rep->generations = generation;
     rep->candidates_enumerated = candidates;
     rep->trace_len = n_levels;
     rep->complete = complete ? 1 : 0;
     rep->upper = U;
-    rep->candidates_visited = visited;
+    rep->candidates_visited = ctl.visited;
     rep->enum_seconds = enum_s;
     rep->n_gammas = G_;
     rep->kernel_launches = launches;

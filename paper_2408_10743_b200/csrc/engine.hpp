@@ -54,9 +54,18 @@ class Plan {
     int sentinel() const { return sentinel_; }
 
    private:
+    // host-side launch description of one level, built the first time a run reaches it
+    struct LevelHost {
+        bool ready = false;
+        int t = 0;                    // 0: walk kernel, else the tile kernel's tail size
+        LevelLaunch walk{};
+        TilePlan tile{};
+    };
+
     void upload();
     long long lower_bound(int g) const;
-    int pick_W_and_pack();
+    void prepare_level(int g);
+    cudaEvent_t level_event(int i);
 
     std::vector<GammaIn> gammas_;
     Mode mode_;
@@ -69,14 +78,16 @@ class Plan {
     std::vector<unsigned long long> h_binom_;
     int device_ = 0, num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
-    bool own_stream_ = true;
-    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     void *d_mem_ = nullptr;
+    size_t d_bytes_ = 0;
     ProblemDev pd_{};
-    std::vector<unsigned char> h_state_;
-    unsigned long long *d_cum_ = nullptr;      // [G * (N + 1) + 1] tile unit table
-    unsigned long long *d_counter_ = nullptr;  // tile unit dispenser
-    std::vector<unsigned long long> h_cum_;
+    std::vector<LevelHost> levels_;             // [N + 1]
+    std::vector<cudaEvent_t> events_;           // 2 per level: before the level kernel, after its close
+    unsigned long long *d_counters_ = nullptr;  // [N + 1] tile unit dispensers, one per level
+    unsigned long long *d_counter_init_ = nullptr;
+    unsigned long long *d_tables_ = nullptr;    // tile unit tables of all levels, back to back
+    size_t table_cap_ = 0, table_used_ = 0;
+    std::vector<unsigned long long> h_counter_init_, h_table_;
 };
 
 // Host cost model for one level: 0 = lexicographic-walk kernel, else the tail size t of

@@ -64,8 +64,56 @@ __device__ __forceinline__ bool admissible_combo(const unsigned long long *syn, 
     return false;
 }
 
+__device__ __forceinline__ bool run_done(const ProblemDev &p) { return *(volatile int *)&p.ctl->done != 0; }
+
+// threshold at kernel start: weights <= U - 1 can still lower U (engine units)
+__device__ __forceinline__ unsigned start_threshold(const ProblemDev &p, unsigned thr0) {
+    const unsigned U = *(volatile unsigned *)&p.ctl->U;
+    return min(min(thr0, U - 1u), *(volatile unsigned *)&p.state->wmin);
+}
+
+__global__ void run_init_kernel(ProblemDev p, unsigned sentinel, const unsigned long long *counter_init,
+                                unsigned long long *counters, int n_counters) {
+    if (threadIdx.x == 0) {
+        p.ctl->U = sentinel;
+        p.ctl->done = 0;
+        p.ctl->best_g = -1;
+        p.ctl->best_key = ~0ull;
+        p.ctl->visited = 0;
+        p.state->wmin = ~0u;
+        p.state->visited = 0;
+    }
+    for (int i = threadIdx.x; i <= p.max_weight; i += blockDim.x) p.key_by_w[i] = ~0ull;
+    for (int i = threadIdx.x; i <= p.N; i += blockDim.x) p.trace_upper[i] = -1;
+    for (int i = threadIdx.x; i < n_counters; i += blockDim.x) counters[i] = counter_init[i];
+}
+
+// Reference run_bz level barrier (engine.cpp:327-335): U from the level minimum (admissible
+// candidates only, already filtered in the kernels), trace entry, stop when L >= U.
+__global__ void level_close_kernel(ProblemDev p, int g, long long lower) {
+    if (threadIdx.x == 0) {
+        RunCtl *c = p.ctl;
+        if (!c->done) {
+            const unsigned w = p.state->wmin;
+            if (w != ~0u && w < c->U) {
+                c->U = w;
+                c->best_g = g;
+                c->best_key = p.key_by_w[w];
+            }
+            p.trace_upper[g] = int(c->U);
+            c->visited += p.state->visited;
+            if (lower >= (long long)c->U) c->done = 1;
+        }
+        p.state->wmin = ~0u;
+        p.state->visited = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i <= p.max_weight; i += blockDim.x) p.key_by_w[i] = ~0ull;
+}
+
 template <int W>
 __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) {
+    if (run_done(p)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowlen = 2 * W;
     const int nrow_words = p.G * p.N * rowlen;
@@ -81,7 +129,7 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
     __syncthreads();
 
     const int g = L.g, N = p.N;
-    unsigned int thr = min(L.thr0, *(volatile unsigned int *)&p.state->wmin);
+    unsigned int thr = start_threshold(p, L.thr0);
     unsigned long long visited = 0;
     int c[kMaxLevel];
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -238,19 +286,28 @@ __device__ __forceinline__ unsigned long long lexrank(const int *c, int g, int N
     return per - 1 - s;
 }
 
+// One work unit of the tile kernel, decoded once per CTA and kept in shared memory so the
+// hot loop carries no per-unit registers (they would spill at 64 registers per thread).
+struct TileUnit {
+    int j, b, tcount, pad;
+    unsigned long long t0;      // first tail (colex rank among (t-1)-subsets of (b, N))
+    unsigned long long hbase0;  // first head of the block (colex rank among h-subsets of [0, b))
+};
+
 // Rare path: a candidate whose fast-path lower bound passed the threshold. Rebuilds its
 // element list from the head rank and the tail rank, computes the exact weight from the
 // rows, applies the admissibility syndrome (reference AdmissibilityFilter,
 // engine.cpp:14-29) and publishes (weight, key). Returns the updated threshold.
 template <int W>
-__device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan tp, const uint32_t *grows, int j, int b,
-                                            unsigned long long head_rank, unsigned long long tail_rank,
-                                            unsigned thrH) {
-    const int N = p.N, h = tp.h, t = tp.t, g = tp.g;
+__device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan tp, const uint32_t *s_rows,
+                                            const unsigned long long *s_binom, const TileUnit *un, int head_off,
+                                            int tix, unsigned thrH) {
+    const int N = p.N, h = tp.h, t = tp.t, g = tp.g, j = un->j, b = un->b;
+    const uint32_t *grows = s_rows + j * N * 2 * W;
     int c[kMaxLevel];
-    unrank_colex(head_rank, h, b, p.binom, p.BK, c);
+    unrank_colex(un->hbase0 + head_off, h, b, s_binom, p.BK, c);
     c[h] = b;
-    unrank_colex(tail_rank, t - 1, N - 1 - b, p.binom, p.BK, c + h + 1);
+    unrank_colex(un->t0 + tix, t - 1, N - 1 - b, s_binom, p.BK, c + h + 1);
     for (int k = h + 1; k < g; k++) c[k] += b + 1;
     uint32_t acc[2 * W];
 #pragma unroll
@@ -269,7 +326,7 @@ __device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan t
         if (!adm) return thrH;
     }
     const unsigned long long key =
-        ((unsigned long long)j << kKeyRankBits) | lexrank(c, g, N, p.binom, p.BK, tp.per_gamma);
+        ((unsigned long long)j << kKeyRankBits) | lexrank(c, g, N, s_binom, p.BK, tp.per_gamma);
     atomicMin(&p.state->wmin, wv);
     atomicMin(&p.key_by_w[wv], key);
     return wv;
@@ -291,12 +348,31 @@ __device__ __forceinline__ uint32_t probe_fold(const uint32_t (&hp)[W], const ui
     }
 }
 
+// colex successor of the ascending m-subset e (m >= 1) with the row sum kept in acc:
+// the lowest element that can move up by one moves, the ones below it reset to 0..q-1.
+// rows(i) = base + (off + i) * rowlen; NW words of each row take part.
+template <int NW>
+__device__ __forceinline__ void colex_step(int *e, int m, uint32_t (&acc)[NW], const uint32_t *base, int off,
+                                           int rowlen) {
+    int q = 0;
+    while (q < m - 1 && e[q] + 1 == e[q + 1]) q++;
+    for (int k = 0; k <= q; k++)
+#pragma unroll
+        for (int w = 0; w < NW; w++) acc[w] ^= base[(off + e[k]) * rowlen + w];
+    e[q]++;
+    for (int k = 0; k < q; k++) e[k] = k;
+    for (int k = 0; k <= q; k++)
+#pragma unroll
+        for (int w = 0; w < NW; w++) acc[w] ^= base[(off + e[k]) * rowlen + w];
+}
+
 template <int W>
 __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kernel(ProblemDev p, TilePlan tp) {
     constexpr int H = heads_per_lane(W);
     constexpr int HB = head_block(W);
     constexpr int PW = probe_stride(W);
-    constexpr int HQ = W == 1 ? H : 1;  // partner words are only needed in registers when W = 1
+    constexpr int NW = W == 1 ? 2 : W;  // words of each row the fast path reads
+    if (run_done(p)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowlen = 2 * W;
     const int G = p.G, N = p.N;
@@ -306,149 +382,149 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
     unsigned long long *s_binom = reinterpret_cast<unsigned long long *>(smem + lay.binom);
     const int nbinom = (N + 1) * p.BK;
     uint32_t *s_tp = reinterpret_cast<uint32_t *>(smem + lay.tp);
-    __shared__ unsigned long long s_unit;
+    __shared__ TileUnit s_un;
     __shared__ unsigned long long s_visited;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[i];
     if (threadIdx.x == 0) s_visited = 0;
 
-    const int t = tp.t, h = tp.h;
     const unsigned sshift = p.scale == 2 ? 1u : 0u;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned thrH = min(tp.thr0, *(volatile unsigned int *)&p.state->wmin);
+    const int lane_head = (threadIdx.x >> 5) * (32 * H) + (threadIdx.x & 31) * H;
+    unsigned thrH = start_threshold(p, tp.thr0);
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_unit = atomicAdd(tp.counter, 1ull);
-        __syncthreads();
-        const unsigned long long unit = s_unit;
-        if (unit >= tp.unit_end) break;
-        // (j, b): the last q with cum[q] <= unit
-        int lo = 0, hi = G * tp.nb - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (__ldg(tp.cum + mid) <= unit) lo = mid; else hi = mid - 1;
+        if (threadIdx.x == 0) {
+            const unsigned long long unit = atomicAdd(tp.counter, 1ull);
+            s_un.tcount = 0;
+            if (unit < tp.unit_end) {
+                // (j, b): the last q with cum[q] <= unit
+                int lo = 0, hi = G * tp.nb - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (__ldg(tp.cum + mid) <= unit) lo = mid; else hi = mid - 1;
+                }
+                const int b = tp.h + lo % tp.nb;
+                const unsigned long long u = unit - __ldg(tp.cum + lo);
+                const unsigned long long Hb = binom_at(s_binom, p.BK, b, tp.h);
+                const unsigned long long Tb = binom_at(s_binom, p.BK, N - 1 - b, tp.t - 1);
+                const unsigned long long nT = (Tb + kTailChunk - 1) / kTailChunk;
+                const unsigned long long hc = u / nT, tc = u % nT;
+                s_un.j = lo / tp.nb;
+                s_un.b = b;
+                s_un.t0 = tc * kTailChunk;
+                s_un.tcount = int(min((unsigned long long)kTailChunk, Tb - s_un.t0));
+                s_un.hbase0 = hc * HB;
+                s_un.pad = int(min((unsigned long long)HB, Hb - hc * HB));  // heads in this block
+                s_visited += (unsigned long long)s_un.pad * (unsigned long long)s_un.tcount;
+            }
         }
-        const int j = lo / tp.nb, b = h + lo % tp.nb;
-        const unsigned long long u = unit - __ldg(tp.cum + lo);
-        const unsigned long long Hb = binom_at(s_binom, p.BK, b, h);
-        const unsigned long long Tb = binom_at(s_binom, p.BK, N - 1 - b, t - 1);
-        const unsigned long long nT = (Tb + kTailChunk - 1) / kTailChunk;
-        const unsigned long long hc = u / nT, tc = u % nT;
-        const unsigned long long t0 = tc * kTailChunk;
-        const int tcount = int(min((unsigned long long)kTailChunk, Tb - t0));
-        const uint32_t *grows = s_rows + j * N * rowlen;
-
-        // stage the tail chunk's probe words: {b} + colex (t-1)-subsets of (b, N)
-        for (int i = threadIdx.x; i < tcount; i += blockDim.x) {
-            int e[kMaxLevel];
-            unrank_colex(t0 + i, t - 1, N - 1 - b, s_binom, p.BK, e);
-            constexpr int SW_ = W == 1 ? 2 : W;  // words staged per tail
-            uint32_t acc[SW_];
+        __syncthreads();
+        const int tcount = s_un.tcount;
+        if (tcount == 0) break;
+        const int t = tp.t, h = tp.h;
+        {
+            const int b = s_un.b;
+            const uint32_t *grows = s_rows + s_un.j * N * rowlen;
+            // stage the tail chunk's probe words: {b} + colex (t-1)-subsets of (b, N);
+            // each thread takes a contiguous run and walks it with colex successors
+            const int R = (tcount + blockDim.x - 1) / blockDim.x;
+            const int i0 = threadIdx.x * R, i1 = min(i0 + R, tcount);
+            if (i0 < i1) {
+                int e[kMaxLevel];
+                unrank_colex(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, p.BK, e);
+                uint32_t acc[NW];
 #pragma unroll
-            for (int w = 0; w < SW_; w++) acc[w] = grows[b * rowlen + w];
-            for (int k = 0; k < t - 1; k++)
+                for (int w = 0; w < NW; w++) acc[w] = grows[b * rowlen + w];
+                for (int k = 0; k < t - 1; k++)
 #pragma unroll
-                for (int w = 0; w < SW_; w++) acc[w] ^= grows[(b + 1 + e[k]) * rowlen + w];
-            // odd counts: pad with a duplicate of the last tail (same candidates)
-            const int copies = (i == tcount - 1 && (tcount & 1)) ? 2 : 1;
-            for (int r = 0; r < copies; r++)
+                    for (int w = 0; w < NW; w++) acc[w] ^= grows[(b + 1 + e[k]) * rowlen + w];
+                for (int i = i0;;) {
 #pragma unroll
-                for (int w = 0; w < SW_; w++) s_tp[(i + r) * PW + w] = acc[w];
+                    for (int w = 0; w < NW; w++) s_tp[i * PW + w] = acc[w];
+                    if (i == tcount - 1 && (tcount & 1))  // odd counts: duplicate the last tail
+#pragma unroll
+                        for (int w = 0; w < NW; w++) s_tp[(i + 1) * PW + w] = acc[w];
+                    if (++i >= i1) break;
+                    colex_step<NW>(e, t - 1, acc, grows, b + 1, rowlen);
+                }
+            }
         }
         __syncthreads();
 
         // this lane's heads: H consecutive colex ranks of h-subsets of [0, b)
-        const unsigned long long hbase = hc * HB + (unsigned long long)warp * (32 * H) + lane * H;
-        const int nvalid = hbase >= Hb ? 0 : int(min((unsigned long long)H, Hb - hbase));
-        if (threadIdx.x == 0) {
-            const unsigned long long blk = min((unsigned long long)HB, Hb - hc * HB);
-            s_visited += blk * (unsigned long long)tcount;
-        }
+        const int nvalid = max(0, min(H, s_un.pad - lane_head));
         if (!__any_sync(0xffffffffu, nvalid > 0)) continue;
-        uint32_t hp[H][W], hq[HQ][W];
+        uint32_t hp[H][W], hq[W == 1 ? H : 1][W];
         {
+            const int b = s_un.b;
+            const uint32_t *grows = s_rows + s_un.j * N * rowlen;
             int e[kMaxLevel];
-            uint32_t x[W], z[W];
-#pragma unroll
-            for (int w = 0; w < W; w++) x[w] = z[w] = 0;
+            uint32_t acc[NW];
             if (nvalid > 0) {
-                unrank_colex(hbase, h, b, s_binom, p.BK, e);
+                unrank_colex(s_un.hbase0 + lane_head, h, b, s_binom, p.BK, e);
+#pragma unroll
+                for (int w = 0; w < NW; w++) acc[w] = 0;
                 for (int k = 0; k < h; k++)
 #pragma unroll
-                    for (int w = 0; w < W; w++) {
-                        x[w] ^= grows[e[k] * rowlen + w];
-                        z[w] ^= grows[e[k] * rowlen + W + w];
-                    }
+                    for (int w = 0; w < NW; w++) acc[w] ^= grows[e[k] * rowlen + w];
             } else {
                 // lanes without heads: all-ones probe words, the fold never passes the check
 #pragma unroll
-                for (int w = 0; w < W; w++) x[w] = z[w] = 0xffffffffu;
+                for (int w = 0; w < NW; w++) acc[w] = 0xffffffffu;
             }
 #pragma unroll
             for (int i = 0; i < H; i++) {
-                if (i > 0 && i < nvalid) {
-                    // colex successor: lowest element that can move up by one
-                    int q = 0;
-                    while (q < h - 1 && e[q] + 1 == e[q + 1]) q++;
-                    for (int k = 0; k <= q; k++)
-#pragma unroll
-                        for (int w = 0; w < W; w++) {
-                            x[w] ^= grows[e[k] * rowlen + w];
-                            if (W == 1) z[w] ^= grows[e[k] * rowlen + W + w];
-                        }
-                    e[q]++;
-                    for (int k = 0; k < q; k++) e[k] = k;
-                    for (int k = 0; k <= q; k++)
-#pragma unroll
-                        for (int w = 0; w < W; w++) {
-                            x[w] ^= grows[e[k] * rowlen + w];
-                            if (W == 1) z[w] ^= grows[e[k] * rowlen + W + w];
-                        }
-                }
+                if (i > 0 && i < nvalid) colex_step<NW>(e, h, acc, grows, 0, rowlen);
                 // heads past the valid count repeat the last valid head (same candidates)
 #pragma unroll
-                for (int w = 0; w < W; w++) {
-                    hp[i][w] = x[w];
-                    if (W == 1) hq[W == 1 ? i : 0][w] = z[w];
-                }
+                for (int w = 0; w < W; w++) hp[i][w] = acc[w];
+                if constexpr (W == 1) hq[i][0] = acc[1];
             }
         }
 
         unsigned thr0 = thrH >> sshift;
-        for (int ti = 0; ti < tcount; ti += 2) {
-            // both tails' probe words: 2 * PW words, whole 16-byte broadcast loads
-            uint32_t tt[2 * PW];
+        int ti = 0;
+        for (;;) {
+            // hot loop: no calls inside, so the heads stay in registers
+            for (; ti < tcount; ti += 2) {
+                // both tails' probe words: 2 * PW words, whole 16-byte broadcast loads
+                uint32_t tt[2 * PW];
 #pragma unroll
-            for (int v = 0; v < 2 * PW; v += 4) {
-                const uint4 q4 = *reinterpret_cast<const uint4 *>(s_tp + ti * PW + v);
-                tt[v] = q4.x;
-                tt[v + 1] = q4.y;
-                tt[v + 2] = q4.z;
-                tt[v + 3] = q4.w;
+                for (int v = 0; v < 2 * PW; v += 4) {
+                    const uint4 q4 = *reinterpret_cast<const uint4 *>(s_tp + ti * PW + v);
+                    tt[v] = q4.x;
+                    tt[v + 1] = q4.y;
+                    tt[v + 2] = q4.z;
+                    tt[v + 3] = q4.w;
+                }
+                unsigned m = 0xffffffffu;
+#pragma unroll
+                for (int i = 0; i < H; i++) {
+                    const unsigned a = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt));
+                    const unsigned c = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt + PW));
+                    m = min(m, min(a, c));
+                }
+                // warp-uniform exit: a lone lane leaving the loop would finish it alone later
+                if (__any_sync(0xffffffffu, m <= thr0 && nvalid > 0)) break;
             }
-            unsigned m = 0xffffffffu;
+            if (ti >= tcount) break;
+            // rare: which of this lane's 2H candidates passed the bound; one call site
+            unsigned fire = 0;
 #pragma unroll
             for (int i = 0; i < H; i++) {
-                const unsigned a = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt));
-                const unsigned c = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt + PW));
-                m = min(m, min(a, c));
-            }
-            if (m <= thr0 && nvalid > 0) {
-                // rare: candidates of this tail pair whose bound passed, exact from the rows
-#pragma unroll 1
-                for (int r = 0; r < 2; r++) {
-                    const int tix = ti + r;
-                    if (tix >= tcount) break;
 #pragma unroll
-                    for (int i = 0; i < H; i++) {
-                        if (i < nvalid &&
-                            __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], s_tp + tix * PW)) <= thr0) {
-                            thrH = tile_exact<W>(p, tp, grows, j, b, hbase + i, t0 + tix, thrH);
-                            thr0 = thrH >> sshift;
-                        }
-                    }
-                }
+                for (int r = 0; r < 2; r++)
+                    if (i < nvalid && ti + r < tcount &&
+                        __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], s_tp + (ti + r) * PW)) <= thr0)
+                        fire |= 1u << (2 * i + r);
             }
+            while (fire) {
+                const int k = __ffs(fire) - 1;
+                fire &= fire - 1;
+                thrH = tile_exact<W>(p, tp, s_rows, s_binom, &s_un, lane_head + (k >> 1), ti + (k & 1), thrH);
+            }
+            thr0 = thrH >> sshift;
+            ti += 2;
         }
         thrH = min(thrH, *(volatile unsigned int *)&p.state->wmin);
     }
@@ -513,6 +589,17 @@ int launch_batch_impl(const BatchDev &b, cudaStream_t st) {
 }  // namespace
 
 size_t problem_smem_bytes(int G, int N, int W, int SW, int BK) { return problem_smem(G, N, W, SW, BK); }
+
+int launch_run_init(const ProblemDev &p, unsigned sentinel, const unsigned long long *counter_init,
+                    unsigned long long *counters, int n_counters, void *stream) {
+    run_init_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, sentinel, counter_init, counters, n_counters);
+    return 1;
+}
+
+int launch_level_close(const ProblemDev &p, int g, long long lower, void *stream) {
+    level_close_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, g, lower);
+    return 1;
+}
 size_t tile_smem_bytes(int G, int N, int W, int SW, int BK) { return tile_smem(G, N, W, SW, BK); }
 
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms) {
