@@ -30,7 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "symplectic-weight combos/sec and time-to-distance, random [[n,k]] codes"
-R_POPC = 16  # POPC results per clock per SM (B200; 15.6 measured, profiles/r01_pipes.log)
+R_POPC = 16  # nominal POPC results per clock per SM
+R_POPC_MEASURED = 15.62  # measured on this pool's B200 (tools/microbench/pipes.cu, profiles/r01_pipes.log)
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 
 
 def parse():
@@ -134,6 +136,16 @@ def cpu_reference_sample(a, levels: int, workers: int) -> dict:
     cands = sum(lv["level_candidates"])
     secs = sum(lv["level_seconds"])
     return dict(candidates=cands, seconds=secs, trace=lv["trace"], prep_seconds=lv["prep_seconds"])
+
+
+def load_profile_summary() -> dict:
+    """Per-launch DRAM traffic of the dominant kernel from the committed ncu --set full
+    capture (profiles/ncu_summary.json, written by tools/ncu_summary.py)."""
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 def cpu_model() -> str:
@@ -259,21 +271,26 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(device)
     n_sm = props.multi_processor_count
     w32 = (c["n"] + 31) // 32
-    per_gpu_peak = n_sm * f_mhz * 1e6 * R_POPC / w32
-    achieved = lvl_cands / lvl_s
-    peak = per_gpu_peak * world
+    achieved = lvl_cands / lvl_s  # candidates/s of the dominant launch, this rank's share x world
+    # XU pipe: the kernel spends exactly one POPC per candidate (one-word probe fold,
+    # DESIGN.md §3), so candidates/s == POPC/s; peak = SMs x SM clock x measured POPC/clk/SM
+    peak = n_sm * f_mhz * 1e6 * R_POPC_MEASURED * world
+    survey_peak = n_sm * f_mhz * 1e6 * R_POPC / w32 * world
+    prof = load_profile_summary()
     roofline = {
-        "bound": "int-pipe POPC (SURVEY.md §8(d)): N_SM x f_SM x 16 / ceil(n/32) candidates/s",
+        "bound": "int-pipe (XU: POPC)",
         "kernel": f"tile_kernel<{w32}> level g={g_last}",
-        "achieved": achieved, "peak": peak, "unit": "cand/s", "frac": achieved / peak,
-        "peak_basis": f"{n_sm} SMs x {f_mhz:.0f} MHz (median under load, nvidia-smi) x {R_POPC} POPC/clk/SM / "
-                      f"{w32} words x {world} GPU(s)",
-        "traffic": None,
-        "note": ("the kernel needs 1 POPC per candidate (OR-fold lower bound, exact rare path), so it can exceed the "
-                 "ceil(n/32)-POPC roofline; its own instruction bound is ALU: 64 LOP3/clk/SM / (2*ceil(n/32)+0.5)"),
-        "alu_peak": n_sm * f_mhz * 1e6 * 64 / (2 * w32 + 0.5) * world,
+        "achieved": achieved, "peak": peak, "unit": "POPC/s (= candidates/s, 1 POPC per candidate)",
+        "frac": achieved / peak,
+        "peak_basis": (f"{n_sm} SMs x {f_mhz:.0f} MHz (median SM clock under load, nvidia-smi) x "
+                       f"{R_POPC_MEASURED} POPC/clk/SM (measured, profiles/r01_pipes.log) x {world} GPU(s)"),
+        "algorithmic_per_launch": f"{lvl_cands} candidates x 1 POPC + 2 LOP3 (W={w32}: {w32} LOP3) + 0.5 VIMNMX3",
+        "traffic": prof.get("dram_bytes_per_launch"),
+        "traffic_note": prof.get("source"),
+        "survey_roofline": {"peak": survey_peak, "frac": achieved / survey_peak,
+                            "basis": "SURVEY.md §8(d): N_SM x f x 16 / ceil(n/32) (ceil(n/32) POPC per candidate); "
+                                     "the probe fold needs 1, so this fraction can exceed 1"},
     }
-    roofline["alu_frac"] = achieved / roofline["alu_peak"]
     plan.close()
 
     # ---------------- e2e: the public C-ABI call, host normalizer in, report out
