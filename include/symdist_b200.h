@@ -91,7 +91,8 @@ typedef struct {
     int world;              /* number of shards (GPUs); 1 = single GPU */
     sdb_allreduce_min_fn allreduce_min;
     void *allreduce_ctx;
-    int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel, 2 force the tile kernel */
+    int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel, 2 force the tile kernel,
+                               3 batch only: run the prep (validation, information sets) on the host */
     void *stream;           /* cudaStream_t to run on (NULL: a private non-blocking stream) */
     int reserved[6];
 } sdb_run_options;

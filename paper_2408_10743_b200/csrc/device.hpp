@@ -71,7 +71,9 @@ struct LevelLaunch {
     unsigned long long per_gamma; // C(N, g)
     unsigned long long seg_len;   // lexicographic ranks per walk segment
     unsigned long long segs_per_gamma;
-    unsigned long long seg_begin, seg_end;  // this rank's shard of [0, G * segs_per_gamma)
+    // sharding: this rank takes segments rank, rank + world, ... of [0, seg_total)
+    unsigned long long seg_total;
+    int shard_rank, shard_world;
 };
 
 // Level-loop control kernels (one CTA each): reset U / best / counters for a run, and
@@ -136,8 +138,11 @@ struct TilePlan {
     unsigned int thr0;              // candidates with weight <= thr0 are considered (U - 1)
     int nb;                         // number of boundaries b in [h, N - t]
     const unsigned long long *cum;  // [G * nb + 1] cumulative unit counts over (j, b)
-    unsigned long long *counter;    // dynamic unit dispenser (starts at unit_begin)
-    unsigned long long unit_begin, unit_end;
+    unsigned long long *counter;    // dynamic dispenser of this rank's units (starts at 0)
+    // sharding: dispensed value i is unit i * shard_world + shard_rank of [0, unit_total);
+    // interleaving keeps neighbouring (similar-sized) units on different ranks
+    unsigned long long unit_total;
+    int shard_rank, shard_world;
     unsigned long long per_gamma;   // C(N, g): lexicographic-rank base
 };
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms);
@@ -153,8 +158,33 @@ struct BatchDev {
     int *out_status;           // [codes] 0 ok, 3 no admissible codeword
     int *out_trace_lower;      // [codes][N]
     int *out_trace_upper;      // [codes][N]
+    const int *in_status;      // [codes] or null: codes with a nonzero prep status are skipped
     int codes, G, N, W, SW, BK, scale, sentinel;
+    int Gs;                    // Gamma slots per code in rows/syn/deficits (>= G)
+    int max_g;                 // last level to run (RunOptions.max_generation; N when 0)
 };
 int launch_batch(const BatchDev &b, void *stream);
+
+// Batch prep on the device, one warp per code (BASELINE config 3):
+// validate_normalizer, isometry_transform, information_sets and the admissibility
+// syndromes with the host's (= reference's) pivot rules, writing the batch kernel's inputs.
+// Limits: n + k <= 64 rows, n <= 64; codes needing more than Gs matrices report G > Gs and
+// the host redoes the batch with host prep.
+constexpr int kPrepMaxRows = 64;
+constexpr int kPrepMaxN = 64;
+constexpr int kPrepGammaSlots = 4;
+struct BatchPrepDev {
+    const unsigned long long *normalizers;  // [codes][N][in_words]
+    int in_words;
+    int codes, N, n, W;
+    int validate, filter;                   // filter: dual_filter && k >= 1
+    uint32_t *rows;                         // [codes][Gs][N][2W]
+    unsigned long long *syn;                // [codes][Gs][N] (filter) — raw N-bit syndromes
+    int *deficits;                          // [codes][Gs]
+    int *n_gammas;                          // [codes]
+    int *status;                            // [codes]: 0 ok, 2 validation
+    int Gs;
+};
+int launch_batch_prep(const BatchPrepDev &d, void *stream);
 
 }  // namespace sdb

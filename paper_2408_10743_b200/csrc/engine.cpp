@@ -391,8 +391,9 @@ void Plan::prepare_level(int g) {
         LL.seg_len = std::max<unsigned long long>(64, seg);
         LL.segs_per_gamma = (per + LL.seg_len - 1) / LL.seg_len;
         const unsigned long long S = LL.segs_per_gamma * (unsigned long long)G_;
-        LL.seg_begin = (unsigned long long)((unsigned __int128)S * rank / world);
-        LL.seg_end = (unsigned long long)((unsigned __int128)S * (rank + 1) / world);
+        LL.seg_total = S;
+        LL.shard_rank = rank;
+        LL.shard_world = world;
     } else {
         TilePlan &tp = lv.tile;
         tp.g = g;
@@ -412,12 +413,13 @@ void Plan::prepare_level(int g) {
                 acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + kTailChunk - 1) / kTailChunk);
             }
         h_table_[size_t(G_) * tp.nb] = acc;
-        tp.unit_begin = (unsigned long long)((unsigned __int128)acc * rank / world);
-        tp.unit_end = (unsigned long long)((unsigned __int128)acc * (rank + 1) / world);
+        tp.unit_total = acc;
+        tp.shard_rank = rank;
+        tp.shard_world = world;
         tp.cum = d_tables_ + table_used_;
         tp.counter = d_counters_ + g;
         table_used_ += n_entries;
-        h_counter_init_[size_t(g)] = tp.unit_begin;
+        h_counter_init_[size_t(g)] = 0;
         // pageable sources: the copies are staged before cudaMemcpyAsync returns
         check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table_.data(), n_entries * 8,
                                    cudaMemcpyHostToDevice, stream_),
@@ -573,10 +575,162 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
 
 // ------------------------------------------------------------------------------- batch
 
+// Batch with the prep on the device (one warp per code). Returns false, having written
+// nothing, when some code needs more Gamma slots than the prep kernel keeps (the caller then
+// runs the host-prep path).
+static bool run_batch_device(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words,
+                             const sdb_run_options &o, int *distances, int *statuses, int *generations,
+                             sdb_trace_entry *traces, int *trace_lens, int trace_cap, double *device_seconds) {
+    const int n = n_cols / 2, k = n_rows - n, N = n_rows, W = (n + 31) / 32;
+    const int Gs = kPrepGammaSlots, SW = (o.dual_filter && k >= 1) ? 1 : 0, BK = std::min(N, kMaxLevel) + 2;
+    check_cuda(cudaSetDevice(o.device), "cudaSetDevice");
+    cudaStream_t st = o.stream ? static_cast<cudaStream_t>(o.stream) : thread_stream(o.device);
+    const std::vector<unsigned long long> h_binom = binom_table(N, BK);
+    const size_t nc = size_t(n_codes);
+    const size_t b_in = align256(nc * N * row_words * 8), b_rows = align256(nc * Gs * N * 2 * W * 4),
+                 b_syn = align256(std::max<size_t>(nc * Gs * N * SW, 1) * 8), b_def = align256(nc * Gs * 4),
+                 b_int = align256(nc * 4), b_binom = align256(h_binom.size() * 8), b_tr = align256(nc * N * 4);
+    const size_t bytes = b_in + b_rows + b_syn + b_def + 5 * b_int + b_binom + 2 * b_tr;
+    void *mem = workspace_get(o.device, bytes);
+    struct Release {
+        int dev;
+        size_t bytes;
+        void *p;
+        cudaStream_t st;
+        ~Release() {
+            cudaStreamSynchronize(st);
+            workspace_put(dev, bytes, p);
+        }
+    } release{o.device, bytes, mem, st};
+    unsigned char *q = static_cast<unsigned char *>(mem);
+    auto take = [&q](size_t b) {
+        unsigned char *p = q;
+        q += b;
+        return p;
+    };
+    BatchPrepDev pd{};
+    pd.normalizers = reinterpret_cast<const unsigned long long *>(take(b_in));
+    pd.rows = reinterpret_cast<uint32_t *>(take(b_rows));
+    pd.syn = reinterpret_cast<unsigned long long *>(take(b_syn));
+    pd.deficits = reinterpret_cast<int *>(take(b_def));
+    pd.n_gammas = reinterpret_cast<int *>(take(b_int));
+    pd.status = reinterpret_cast<int *>(take(b_int));
+    BatchDev bd{};
+    bd.out_upper = reinterpret_cast<int *>(take(b_int));
+    bd.out_generations = reinterpret_cast<int *>(take(b_int));
+    bd.out_status = reinterpret_cast<int *>(take(b_int));
+    bd.binom = reinterpret_cast<const unsigned long long *>(take(b_binom));
+    bd.out_trace_lower = reinterpret_cast<int *>(take(b_tr));
+    bd.out_trace_upper = reinterpret_cast<int *>(take(b_tr));
+    pd.in_words = row_words;
+    pd.codes = n_codes;
+    pd.N = N;
+    pd.n = n;
+    pd.W = W;
+    pd.validate = o.validate;
+    pd.filter = SW;
+    pd.Gs = Gs;
+    check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(pd.normalizers), rows, nc * N * row_words * 8,
+                               cudaMemcpyHostToDevice, st),
+               "H2D normalizers");
+    check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(bd.binom), h_binom.data(), h_binom.size() * 8,
+                               cudaMemcpyHostToDevice, st),
+               "H2D binom");
+    cudaEvent_t e0 = event_get(o.device), e1 = event_get(o.device);
+    check_cuda(cudaEventRecord(e0, st), "event");
+    launch_batch_prep(pd, st);
+    check_cuda(cudaGetLastError(), "batch prep launch");
+    std::vector<int> ng(nc), pst(nc);
+    check_cuda(cudaMemcpyAsync(ng.data(), pd.n_gammas, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaMemcpyAsync(pst.data(), pd.status, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaStreamSynchronize(st), "batch prep sync");
+    int G = 0;
+    for (size_t c = 0; c < nc; c++)
+        if (pst[c] == 0) G = std::max(G, ng[c]);
+    if (G > Gs) {
+        event_put(o.device, e0);
+        event_put(o.device, e1);
+        return false;
+    }
+    for (int c = 0; c < n_codes; c++) {
+        distances[c] = -1;
+        generations[c] = 0;
+        trace_lens[c] = 0;
+        statuses[c] = pst[size_t(c)] == 0 ? 0 : SDB_ERR_VALIDATION;
+    }
+    if (G > 0) {
+        bd.rows = pd.rows;
+        bd.syn = pd.syn;
+        bd.deficits = pd.deficits;
+        bd.in_status = pd.status;
+        bd.codes = n_codes;
+        bd.G = G;
+        bd.Gs = Gs;
+        bd.N = N;
+        bd.W = W;
+        bd.SW = SW;
+        bd.BK = BK;
+        bd.scale = 2;
+        bd.sentinel = 3 * n + 1;
+        bd.max_g = o.max_generation;
+        if (problem_smem_bytes(G, N, W, SW, BK) > 200 * 1024) throw InvalidArgument("batch codes too large");
+        if (launch_batch(bd, st) < 0) throw InvalidArgument("unsupported row width");
+        check_cuda(cudaGetLastError(), "batch kernel launch");
+        check_cuda(cudaEventRecord(e1, st), "event");
+        std::vector<int> up(nc), gen(nc), stt(nc), tl(nc * N), tu(nc * N);
+        check_cuda(cudaMemcpyAsync(up.data(), bd.out_upper, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(gen.data(), bd.out_generations, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(stt.data(), bd.out_status, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(tl.data(), bd.out_trace_lower, nc * N * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(tu.data(), bd.out_trace_upper, nc * N * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaStreamSynchronize(st), "batch sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (device_seconds) *device_seconds = ms * 1e-3;
+        for (int c = 0; c < n_codes; c++) {
+            if (statuses[c] != 0) continue;
+            const size_t cc = size_t(c);
+            generations[c] = gen[cc];
+            trace_lens[c] = gen[cc];
+            for (int g = 0; g < gen[cc] && g < trace_cap; g++)
+                traces[cc * trace_cap + g] = sdb_trace_entry{g + 1, tl[cc * N + g], tu[cc * N + g]};
+            if (stt[cc] != 0 || up[cc] % 2 != 0)
+                statuses[c] = SDB_ERR_INTERNAL;
+            else
+                distances[c] = up[cc] / 2;
+        }
+    } else if (device_seconds) {
+        *device_seconds = 0;
+    }
+    event_put(o.device, e0);
+    event_put(o.device, e1);
+    return true;
+}
+
 void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
                int *distances, int *statuses, int *generations, sdb_trace_entry *traces, int *trace_lens,
                int trace_cap, double *device_seconds) {
     if (n_codes <= 0) return;
+    if (n_cols % 2 != 0 || n_cols == 0)
+        throw InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+    {
+        const int n = n_cols / 2, k = n_rows - n;
+        // validate_normalizer's shape checks (distance.cpp:71-79) are per batch: one shape
+        if (o.validate && (n_rows == 0 || k < 0 || n_rows > 2 * n)) {
+            for (int c = 0; c < n_codes; c++) {
+                statuses[c] = SDB_ERR_VALIDATION;
+                distances[c] = -1;
+                generations[c] = 0;
+                trace_lens[c] = 0;
+            }
+            if (device_seconds) *device_seconds = 0;
+            return;
+        }
+        if (o.kernel != 3 && n_rows >= 1 && n_rows <= kPrepMaxRows && n <= kPrepMaxN &&
+            run_batch_device(rows, n_codes, n_rows, n_cols, row_words, o, distances, statuses, generations, traces,
+                             trace_lens, trace_cap, device_seconds))
+            return;
+    }
     if (n_cols % 2 != 0 || n_cols == 0)
         throw InvalidArgument("StabilizerInstance: column count must be even and nonzero");
     const int n = n_cols / 2, k = n_rows - n, N = n_rows;
@@ -686,6 +840,9 @@ void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int ro
     bd.BK = BK;
     bd.scale = 2;
     bd.sentinel = 3 * n + 1;
+    bd.Gs = G;
+    bd.in_status = nullptr;
+    bd.max_g = o.max_generation;
     try {
         check_cuda(cudaMemcpyAsync(base, h_rows.data(), h_rows.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
         if (!h_syn.empty())

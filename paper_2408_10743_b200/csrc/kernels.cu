@@ -133,8 +133,9 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
     unsigned long long visited = 0;
     int c[kMaxLevel];
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long seg = L.seg_begin + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-         seg < L.seg_end; seg += stride) {
+    for (unsigned long long it = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;; it += stride) {
+        const unsigned long long seg = it * L.shard_world + L.shard_rank;
+        if (seg >= L.seg_total) break;
         const int j = int(seg / L.segs_per_gamma);
         const unsigned long long r0 = (seg % L.segs_per_gamma) * L.seg_len;
         const unsigned long long r1 = min(r0 + L.seg_len, L.per_gamma);
@@ -189,8 +190,16 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     const int nsyn = G * N * b.SW;
     __shared__ unsigned int s_wmin;
     __shared__ int s_done;
-    const uint32_t *grow = b.rows + (size_t)code * nrow_words;
-    const unsigned long long *gsyn = b.syn + (size_t)code * nsyn;
+    if (b.in_status && b.in_status[code] != 0) {
+        if (threadIdx.x == 0) {
+            b.out_upper[code] = b.sentinel;
+            b.out_generations[code] = 0;
+            b.out_status[code] = b.in_status[code];
+        }
+        return;
+    }
+    const uint32_t *grow = b.rows + (size_t)code * b.Gs * N * rowlen;
+    const unsigned long long *gsyn = b.syn + (size_t)code * b.Gs * N * b.SW;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = grow[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = b.binom[i];
     for (int i = threadIdx.x; i < nsyn; i += blockDim.x) s_syn[i] = gsyn[i];
@@ -200,7 +209,8 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     int U = b.sentinel;
     int gen = 0;
     int c[kMaxLevel];
-    for (int g = 1; g <= N; g++) {
+    const int g_last = b.max_g > 0 ? min(N, b.max_g) : N;
+    for (int g = 1; g <= g_last; g++) {
         const unsigned long long per = binom_at(s_binom, b.BK, N, g);
         // ~32 candidates per thread per segment keeps every thread busy on tiny levels
         const unsigned long long total = per * G;
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
             if (int(s_wmin) < U) U = int(s_wmin);
             long lower = 0;
             for (int j = 0; j < G; j++) {
-                const int t = g + 1 - b.deficits[(size_t)code * G + j];
+                const int t = g + 1 - b.deficits[(size_t)code * b.Gs + j];
                 lower += t > 0 ? t : 0;
             }
             b.out_trace_lower[(size_t)code * N + g - 1] = int(lower);
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     if (threadIdx.x == 0) {
         b.out_upper[code] = U;
         b.out_generations[code] = gen;
-        b.out_status[code] = U >= b.sentinel ? 3 : 0;
+        b.out_status[code] = (U >= b.sentinel && (s_done || gen == N)) ? 3 : 0;
     }
 }
 
@@ -394,9 +404,9 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned long long unit = atomicAdd(tp.counter, 1ull);
+            const unsigned long long unit = atomicAdd(tp.counter, 1ull) * tp.shard_world + tp.shard_rank;
             s_un.tcount = 0;
-            if (unit < tp.unit_end) {
+            if (unit < tp.unit_total) {
                 // (j, b): the last q with cum[q] <= unit
                 int lo = 0, hi = G * tp.nb - 1;
                 while (lo < hi) {
@@ -544,7 +554,7 @@ int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, i
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<W>, kTileThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    const unsigned long long units = tp.unit_end - tp.unit_begin;
+    const unsigned long long units = (tp.unit_total + tp.shard_world - 1 - tp.shard_rank) / tp.shard_world;
     unsigned long long blocks = (unsigned long long)num_sms * per_sm;
     if (blocks > units) blocks = units;
     if (blocks == 0) return 0;
@@ -564,7 +574,7 @@ int launch_walk_impl(const ProblemDev &p, const LevelLaunch &L, cudaStream_t st,
         cudaFuncSetAttribute(walk_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
-    const unsigned long long segs = L.seg_end - L.seg_begin;
+    const unsigned long long segs = (L.seg_total + L.shard_world - 1 - L.shard_rank) / L.shard_world;
     const int threads = 256;
     unsigned long long blocks = (segs + threads - 1) / threads;
     const unsigned long long cap = (unsigned long long)num_sms * 8;

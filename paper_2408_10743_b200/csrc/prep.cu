@@ -1,0 +1,299 @@
+// Batch prep on the device (BASELINE config 3): one warp per code
+// runs the host prep of the isometry route — validate_normalizer (distance.cpp:71-93),
+// isometry_transform (prep.cpp:299-315), information_sets (prep.cpp:317-364) and the
+// admissibility syndromes (engine.cpp:14-29) — and writes the batch kernel's inputs.
+//
+// Rows live in registers, two per lane (row i: lane i % 32, slot i / 32). Every elimination
+// step is warp-uniform: a ballot finds the pivot row (first row >= r with a 1 in column c,
+// exactly the host's and the reference's rule), shuffles broadcast it, and each lane XORs it
+// into its own rows. So the Gamma_j — and the bound trace — are the host's bit for bit.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.hpp"
+
+namespace sdb {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// image rows: 3n <= 192 columns -> 3 words; normalizer rows: 2n <= 128 -> 2 words
+template <int NW>
+struct WarpRows {
+    unsigned long long v[2][NW];  // rows lane and lane + 32
+
+    __device__ __forceinline__ bool bit(int slot, int c) const { return (v[slot][c >> 6] >> (c & 63)) & 1ull; }
+
+    // row i broadcast to every lane (i warp-uniform)
+    __device__ __forceinline__ void fetch(int i, unsigned long long (&out)[NW]) const {
+        const int slot = i >> 5, src = i & 31;
+#pragma unroll
+        for (int w = 0; w < NW; w++) out[w] = __shfl_sync(kFull, slot ? v[1][w] : v[0][w], src);
+    }
+
+    // one step of the reference's elimination (bitvec.cpp:213-233 / prep.cpp:330-346): the
+    // first row sel >= r with a 1 in column c becomes row r and is XORed into every other
+    // row with a 1 there. Returns false when no row qualifies.
+    __device__ __forceinline__ bool pivot(int c, int r, int rows) {
+        const int lane = threadIdx.x & 31;
+        const unsigned b0 = __ballot_sync(kFull, lane < rows && lane >= r && bit(0, c));
+        const unsigned b1 = __ballot_sync(kFull, lane + 32 < rows && lane + 32 >= r && bit(1, c));
+        if (!(b0 | b1)) return false;
+        const int sel = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
+        unsigned long long prow[NW], rrow[NW];
+        fetch(sel, prow);
+        fetch(r, rrow);
+        if (sel != r) {
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                const int i = lane + 32 * s;
+                if (i == r)
+#pragma unroll
+                    for (int w = 0; w < NW; w++) v[s][w] = prow[w];
+                else if (i == sel)
+#pragma unroll
+                    for (int w = 0; w < NW; w++) v[s][w] = rrow[w];
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+            const int i = lane + 32 * s;
+            if (i < rows && i != r && bit(s, c))
+#pragma unroll
+                for (int w = 0; w < NW; w++) v[s][w] ^= prow[w];
+        }
+        return true;
+    }
+};
+
+// columns [from, from + len) of a packed NW-word row, len <= 64
+template <int NW>
+__device__ __forceinline__ unsigned long long bits_at(const unsigned long long (&w)[NW], int from, int len) {
+    const int wi = from >> 6, sh = from & 63;
+    unsigned long long x = 0;
+#pragma unroll
+    for (int i = 0; i < NW; i++)
+        if (i == wi) x = w[i] >> sh;
+    if (sh)
+#pragma unroll
+        for (int i = 1; i < NW; i++)
+            if (i == wi + 1) x |= w[i] << (64 - sh);
+    return len == 64 ? x : (x & ((1ull << len) - 1));
+}
+
+__global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
+    const int lane = threadIdx.x & 31;
+    const int code = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (code >= d.codes) return;
+    const int N = d.N, n = d.n;
+    __shared__ unsigned char s_piv[4][3 * kPrepMaxN];
+    unsigned char *piv = s_piv[threadIdx.x >> 5];
+
+    // ---- load the normalizer (a|b): row i of this code
+    WarpRows<2> A;
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+        const int i = lane + 32 * s;
+#pragma unroll
+        for (int w = 0; w < 2; w++)
+            A.v[s][w] = (i < N && w < d.in_words) ? d.normalizers[((size_t)code * N + i) * d.in_words + w] : 0ull;
+    }
+    // mask padding bits beyond 2n
+#pragma unroll
+    for (int s = 0; s < 2; s++)
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+            const int lo = 64 * w, hi = min(2 * n, 64 * w + 64);
+            if (hi <= lo) A.v[s][w] = 0;
+            else if (hi - lo < 64) A.v[s][w] &= (1ull << (hi - lo)) - 1;
+        }
+    int status = 0;
+
+    // ---- validate_normalizer (distance.cpp:71-93); shape checks are done on the host
+    if (d.validate) {
+        WarpRows<2> E = A;  // echelon form of A (rank, in_rowspace)
+        int r = 0;
+        for (int c = 0; c < 2 * n && r < N; c++)
+            if (E.pivot(c, r, N)) piv[r++] = (unsigned char)c;
+        const int rankA = r;
+        if (rankA != N) {
+            status = 2;
+        } else {
+            // symplectic dual = Euclidean kernel of the half-swapped rows (bitvec.cpp:261-274)
+            WarpRows<2> S;
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                const unsigned long long a = bits_at(A.v[s], 0, n), b = bits_at(A.v[s], n, n);
+                // (b | a) packed at columns [0, n) and [n, 2n)
+                unsigned long long lo = b, hi = 0;
+                if (n < 64) {
+                    lo |= a << n;
+                    hi = n == 0 ? 0 : (a >> (64 - n));
+                } else {
+                    hi = a;
+                }
+                S.v[s][0] = lo;
+                S.v[s][1] = 2 * n > 64 ? hi : 0;
+            }
+            __shared__ unsigned char s_spiv[4][2 * kPrepMaxN];
+            unsigned char *spiv = s_spiv[threadIdx.x >> 5];
+            int rs = 0;
+            for (int c = 0; c < 2 * n && rs < N; c++)
+                if (S.pivot(c, rs, N)) spiv[rs++] = (unsigned char)c;
+            // free columns in ascending order; dual vector f: e_f + sum_r S[r][f] e_{spiv[r]}
+            // two free columns per lane (n - k <= 64)
+            unsigned long long dv[2][2] = {{0, 0}, {0, 0}};
+            int fcol[2] = {-1, -1};
+            {
+                int nf = 0, pi = 0;
+                for (int c = 0; c < 2 * n; c++) {
+                    if (pi < rs && spiv[pi] == c) { pi++; continue; }
+                    if ((nf & 31) == lane) fcol[nf >> 5] = c;
+                    nf++;
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < 2; s++)
+                if (fcol[s] >= 0) dv[s][fcol[s] >> 6] |= 1ull << (fcol[s] & 63);
+            for (int q = 0; q < rs; q++) {
+                unsigned long long row[2];
+                S.fetch(q, row);
+#pragma unroll
+                for (int s = 0; s < 2; s++)
+                    if (fcol[s] >= 0 && ((row[fcol[s] >> 6] >> (fcol[s] & 63)) & 1ull))
+                        dv[s][spiv[q] >> 6] |= 1ull << (spiv[q] & 63);
+            }
+            // in_rowspace(A, v): reduce by the echelon rows of A
+            for (int q = 0; q < rankA; q++) {
+                unsigned long long row[2];
+                E.fetch(q, row);
+                const int pc = piv[q];
+#pragma unroll
+                for (int s = 0; s < 2; s++)
+                    if ((dv[s][pc >> 6] >> (pc & 63)) & 1ull) {
+                        dv[s][0] ^= row[0];
+                        dv[s][1] ^= row[1];
+                    }
+            }
+            const bool bad = (dv[0][0] | dv[0][1] | dv[1][0] | dv[1][1]) != 0;
+            if (__any_sync(kFull, bad)) status = 2;
+        }
+    }
+
+    // ---- isometry_transform: (a | b | a^b) in 3n <= 192 columns
+    WarpRows<3> cur;
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+        const unsigned long long a = bits_at(A.v[s], 0, n), b = bits_at(A.v[s], n, n), c = a ^ b;
+        unsigned long long out[3] = {0, 0, 0};
+        // place a at 0, b at n, c at 2n
+        const unsigned long long parts[3] = {a, b, c};
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            const int from = p * n, wi = from >> 6, sh = from & 63;
+            out[wi] |= parts[p] << sh;
+            if (sh && wi + 1 < 3 && n > 64 - sh) out[wi + 1] |= parts[p] >> (64 - sh);
+        }
+#pragma unroll
+        for (int w = 0; w < 3; w++) cur.v[s][w] = out[w];
+    }
+
+    // ---- information_sets (prep.cpp:317-364): greedy elimination on unused columns, cur
+    // carried over between matrices, rank_deficit = rows - pivots
+    unsigned long long used[3] = {0, 0, 0};
+    unsigned long long gx[kPrepGammaSlots][2], gz[kPrepGammaSlots][2];
+#pragma unroll
+    for (int j = 0; j < kPrepGammaSlots; j++) gx[j][0] = gx[j][1] = gz[j][0] = gz[j][1] = 0;
+    int G = 0;
+    const int W = d.W, rowlen = 2 * d.W;
+    for (; status == 0;) {
+        int r = 0;
+        for (int c = 0; c < 3 * n && r < N; c++) {
+            if ((used[c >> 6] >> (c & 63)) & 1ull) continue;
+            if (cur.pivot(c, r, N)) piv[r++] = (unsigned char)c;
+        }
+        if (r == 0) break;
+        if (G == 0 && r != N) {  // information_sets: rows are linearly dependent
+            status = 2;
+            break;
+        }
+        if (G < d.Gs) {
+            // rows of Gamma_G: x = columns [0, n), z = columns [n, 2n) of the image
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                const unsigned long long x = bits_at(cur.v[s], 0, n), z = bits_at(cur.v[s], n, n);
+#pragma unroll
+                for (int j = 0; j < kPrepGammaSlots; j++)
+                    if (j == G) {
+                        gx[j][s] = x;
+                        gz[j][s] = z;
+                    }
+                const int i = lane + 32 * s;
+                if (i >= N) continue;
+                uint32_t *dst = d.rows + (((size_t)code * d.Gs + G) * N + i) * rowlen;
+                for (int w = 0; w < W; w++) {
+                    dst[w] = uint32_t(x >> (32 * w));
+                    dst[W + w] = uint32_t(z >> (32 * w));
+                }
+            }
+            if (lane == 0) d.deficits[(size_t)code * d.Gs + G] = N - r;
+        }
+        for (int q = 0; q < r; q++) used[piv[q] >> 6] |= 1ull << (piv[q] & 63);
+        G++;
+    }
+
+    // ---- admissibility syndromes: bit f of row i = <first 2n columns of row i, A_f>_s;
+    // N <= 64 so the raw syndrome is one word (zero iff the compressed one is zero)
+    if (status == 0 && d.filter) {
+        unsigned long long syn[kPrepGammaSlots][2];
+#pragma unroll
+        for (int j = 0; j < kPrepGammaSlots; j++) syn[j][0] = syn[j][1] = 0;
+        for (int f = 0; f < N; f++) {
+            unsigned long long arow[2];
+            A.fetch(f, arow);
+            const unsigned long long fa = bits_at(arow, 0, n), fb = bits_at(arow, n, n);
+#pragma unroll
+            for (int j = 0; j < kPrepGammaSlots; j++)
+#pragma unroll
+                for (int s = 0; s < 2; s++)
+                    syn[j][s] |= (unsigned long long)((__popcll(gx[j][s] & fb) + __popcll(gz[j][s] & fa)) & 1) << f;
+        }
+        const int gs = min(G, d.Gs);
+#pragma unroll
+        for (int j = 0; j < kPrepGammaSlots; j++)
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                const int i = lane + 32 * s;
+                if (j < gs && i < N) d.syn[((size_t)code * d.Gs + j) * N + i] = syn[j][s];
+            }
+    }
+    // pad unused slots with Gamma_0 and a deficit that never reaches L (duplicates cannot
+    // lower the minimum)
+    if (status == 0 && G > 0)
+        for (int j = G; j < d.Gs; j++) {
+            for (int i = lane; i < N; i += 32) {
+                const uint32_t *src = d.rows + (((size_t)code * d.Gs) * N + i) * rowlen;
+                uint32_t *dst = d.rows + (((size_t)code * d.Gs + j) * N + i) * rowlen;
+                for (int w = 0; w < rowlen; w++) dst[w] = src[w];
+                if (d.filter) d.syn[((size_t)code * d.Gs + j) * N + i] = d.syn[((size_t)code * d.Gs) * N + i];
+            }
+            if (lane == 0) d.deficits[(size_t)code * d.Gs + j] = 1 << 20;
+        }
+    if (lane == 0) {
+        d.status[code] = status;
+        d.n_gammas[code] = G;
+    }
+}
+
+}  // namespace
+
+int launch_batch_prep(const BatchPrepDev &d, void *stream) {
+    if (d.codes <= 0) return 0;
+    const int warps = 4;
+    batch_prep_kernel<<<(d.codes + warps - 1) / warps, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
+    return 1;
+}
+
+}  // namespace sdb

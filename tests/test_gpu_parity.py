@@ -192,3 +192,46 @@ def test_engine_kats_forced_kernels(gpu, kernel):
         ham = gpu.run_bz([gpu.singleton_gamma(gpu.isometry_transform(m), gpu.WeightMode.hamming)],
                          gpu.AdmissibilityFilter.disabled(), opts=o)
         assert ham.trace == [tuple(t) for t in case["hamming"]["trace"]]
+
+
+def test_batch_host_prep_path_matches_device_prep(gpu):
+    # kernel=3 forces the host prep (validation, isometry, information sets on the CPU);
+    # the default batch path runs them on the device, one warp per code
+    gd = load_golden("config3.json")
+    codes = [gpu.generate_code(gd["n"], gd["k"], c["seed"]) for c in gd["codes"][:512]]
+    dev = gpu.saved_isometry_batch(codes)
+    host = gpu.saved_isometry_batch(codes, gpu.RunOptions(kernel=3))
+    assert (dev.statuses == 0).all() and (host.statuses == 0).all()
+    assert (dev.distances == host.distances).all()
+    assert dev.traces == host.traces == [[tuple(t) for t in c["trace"]] for c in gd["codes"][:512]]
+
+
+def test_batch_device_prep_rejects_what_the_host_rejects(gpu):
+    rng = np.random.default_rng(5)
+    good = [gpu.generate_code(12, 3, s) for s in range(1, 9)]
+    dep = good[0].copy()
+    dep[1] = dep[0]                                   # dependent rows
+    rnd = rng.integers(0, 2, size=(15, 24), dtype=np.uint8)  # random rows: not a normalizer
+    batch = good[:3] + [dep, rnd] + good[3:]
+    for filt in (True, False):
+        for validate in (True, False):
+            o = gpu.RunOptions(validate=validate, dual_filter=filt)
+            dev = gpu.saved_isometry_batch(batch, o)
+            host = gpu.saved_isometry_batch(batch, gpu.RunOptions(validate=validate, dual_filter=filt, kernel=3))
+            assert (dev.statuses == host.statuses).all(), (validate, filt, dev.statuses, host.statuses)
+            ok = dev.statuses == 0
+            assert (dev.distances[ok] == host.distances[ok]).all()
+            assert [t for t, g in zip(dev.traces, ok) if g] == [t for t, g in zip(host.traces, ok) if g]
+    st = gpu.saved_isometry_batch(batch).statuses
+    assert st[3] == 2 and st[4] == 2 and (np.delete(st, [3, 4]) == 0).all()
+
+
+@pytest.mark.parametrize("nk", [(30, 4), (40, 6), (64, 0), (33, 31), (62, 2)])
+def test_batch_device_prep_shapes(gpu, nk):
+    # multi-word rows (n > 32), k = 0 (filter off), n + k = 64 rows (two rows per lane)
+    n, k = nk
+    codes = [gpu.generate_code(n, k, s) for s in range(100, 104)]
+    dev = gpu.saved_isometry_batch(codes, gpu.RunOptions(max_generation=3) if n > 40 else None)
+    host = gpu.saved_isometry_batch(codes, gpu.RunOptions(kernel=3, max_generation=3 if n > 40 else 0))
+    assert (dev.statuses == host.statuses).all()
+    assert dev.traces == host.traces
