@@ -20,6 +20,14 @@
  *   sdb_validate_normalizer symdist::validate_normalizer include/symdist/distance.hpp:57
  *   sdb_isometry_transform  symdist::isometry_transform  include/symdist/prep.hpp:69
  *   sdb_information_sets    symdist::information_sets    include/symdist/prep.hpp:75
+ *   sdb_saved_1_gamma       symdist::saved_1_gamma       include/symdist/distance.hpp:60
+ *                                                         (src/distance.cpp:95-113)
+ *   sdb_saved_2_gamma       symdist::saved_2_gamma       include/symdist/distance.hpp:64
+ *                                                         (src/distance.cpp:115-133)
+ *   sdb_run_bz_packaged     symdist::run_bz              include/symdist/engine.hpp:60-61
+ *                                                         with 1/3-packages (prep.hpp:13-35)
+ *   sdb_prepare_packages    symdist::diagonalize_f2 / diagonalize_f4 + second_gamma
+ *                                                         include/symdist/prep.hpp:48-64
  *   sdb_saved_isometry_batch  (no reference counterpart: a loop of saved_isometry
  *                              calls, one code per CTA on the GPU; BASELINE config 3)
  *   sdb_generate_code       (BASELINE.md §2 seeded config generator)
@@ -137,9 +145,18 @@ sdb_status sdb_saved_isometry(const uint64_t *rows, int n_rows, int n_cols, int 
                               const sdb_run_options *opts, sdb_report *report,
                               sdb_trace_entry *trace, int trace_cap, uint64_t *best_out);
 
-/* compute_distance dispatch. SDB_ALG_SAVED_ISOMETRY and SDB_ALG_AUTO (k > 2) run the
- * isometry route; the package routes (1Γ/2Γ, and AUTO with k <= 2) and brute force
- * return SDB_ERR_INVALID_ARGUMENT until they land. */
+/* Saved_1_Gamma / Saved_2_Gamma: the package routes, symplectic units (distance = U). best_out
+ * (2n columns, ceil(2n/64) words) is in the prepared frame (Saved_1_Gamma permutes pairs). */
+sdb_status sdb_saved_1_gamma(const uint64_t *rows, int n_rows, int n_cols, int row_words,
+                             const sdb_run_options *opts, sdb_report *report,
+                             sdb_trace_entry *trace, int trace_cap, uint64_t *best_out);
+sdb_status sdb_saved_2_gamma(const uint64_t *rows, int n_rows, int n_cols, int row_words,
+                             const sdb_run_options *opts, sdb_report *report,
+                             sdb_trace_entry *trace, int trace_cap, uint64_t *best_out);
+
+/* compute_distance dispatch (distance.cpp:226-240): AUTO runs Saved_2_Gamma when k <= 2 and
+ * the isometry route otherwise; SDB_ALG_BRUTE_FORCE returns SDB_ERR_INVALID_ARGUMENT (the
+ * brute-force oracle is test infrastructure here, oracle/). */
 sdb_status sdb_compute_distance(const uint64_t *rows, int n_rows, int n_cols, int row_words,
                                 int algorithm, const sdb_run_options *opts, sdb_report *report,
                                 sdb_trace_entry *trace, int trace_cap);
@@ -168,6 +185,18 @@ sdb_status sdb_run_bz(const uint64_t *gammas, int n_gammas, int n_rows, int n_co
                       const sdb_run_options *opts, sdb_report *report, sdb_trace_entry *trace,
                       int trace_cap, uint64_t *best_out);
 
+/* run_bz over packaged matrices (1 or 3 rows per package; reference PackagedGamma). Matrix j
+ * has gamma_rows[j] <= max_rows rows at gammas + j*max_rows*row_words. packages: for each
+ * matrix in turn, n_packages[j] entries of [size, row_0, .., row_{size-1}]. n_pp (may be
+ * NULL: all packages principal) feeds the two-matrix lower bound. */
+sdb_status sdb_run_bz_packaged(const uint64_t *gammas, int n_gammas, const int *gamma_rows, int max_rows,
+                               int n_cols, int row_words, int mode, int pair_count,
+                               const int *rank_deficits, const int *n_packages, const int *n_pp,
+                               const int *packages, const uint64_t *filter_rows, int filter_n_rows,
+                               int filter_n_cols, int filter_row_words, int filter_enabled, int filter_k,
+                               const sdb_run_options *opts, sdb_report *report, sdb_trace_entry *trace,
+                               int trace_cap, uint64_t *best_out);
+
 /* lower_bound(g, gammas) for singleton Hamming / symplectic matrices. */
 sdb_status sdb_lower_bound(int g, int mode, int n_gammas, const int *rank_deficits,
                            const int *n_packages, const int *n_pp, long long *out);
@@ -184,6 +213,14 @@ sdb_status sdb_isometry_transform(const uint64_t *rows, int n_rows, int n_cols, 
 sdb_status sdb_information_sets(const uint64_t *rows, int n_rows, int n_cols, int row_words,
                                 int max_gammas, uint64_t *out, int out_row_words, int *deficits,
                                 int *pivots, int *n_gammas);
+/* The package routes' prepared matrices (algorithm SDB_ALG_SAVED_1_GAMMA: diagonalize_f2;
+ * SDB_ALG_SAVED_2_GAMMA: diagonalize_f4 then second_gamma). Matrix j (gamma_rows[j] rows of
+ * n_cols) at out + j*max_rows*out_row_words; packages encoded as in sdb_run_bz_packaged. */
+sdb_status sdb_prepare_packages(const uint64_t *rows, int n_rows, int n_cols, int row_words, int algorithm,
+                                int max_gammas, int max_rows, uint64_t *out, int out_row_words,
+                                int *gamma_rows, int *n_packages, int *n_pp, int *packages,
+                                int packages_cap, int *n_gammas);
+
 /* BASELINE.md §2 generator: (n+k) x 2n normalizer from seed (xorshift64*), transvections
  * <= 0 means 4n. */
 sdb_status sdb_generate_code(int n, int k, uint64_t seed, int transvections, uint64_t *out,

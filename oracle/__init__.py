@@ -232,6 +232,45 @@ def ref_isometry_best(mat, workers: int = 1) -> dict:
     return dict(upper=upper.value, best=best[: blen.value].copy())
 
 
+def ref_prepare_packages(mat, alg: str) -> list[dict]:
+    """The reference's package-route prep: diagonalize_f2 (saved_1_gamma) or diagonalize_f4 +
+    second_gamma (saved_2_gamma)."""
+    lib = _load(REF_SO)
+    a = _u8(mat)
+    rows, cols = a.shape
+    max_rows = 2 * rows + 2
+    out = np.zeros((2, max_rows, cols), dtype=np.uint8)
+    gr, npk, npp = (np.zeros(2, dtype=np.int32) for _ in range(3))
+    pk = np.zeros(16 * rows + 16, dtype=np.int32)
+    ng = C.c_int(0)
+    err = _err()
+    ip = lambda x: x.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+    rc = lib.ref_prepare_packages(_ptr(a), rows, cols, ALG[alg], max_rows, _ptr(out), ip(gr), ip(npk), ip(npp),
+                                  ip(pk), len(pk), C.byref(ng), err, 512)
+    _check(rc, err)
+    res, pos = [], 0
+    for j in range(ng.value):
+        pkgs = []
+        for _ in range(int(npk[j])):
+            sz = int(pk[pos])
+            pkgs.append([int(x) for x in pk[pos + 1:pos + 1 + sz]])
+            pos += 1 + sz
+        res.append(dict(matrix=out[j, :int(gr[j])].copy(), packages=pkgs, n_pp=int(npp[j])))
+    return res
+
+
+def ref_package_best(mat, alg: str, workers: int = 1) -> dict:
+    lib = _load(REF_SO)
+    a = _u8(mat)
+    best = np.zeros(a.shape[1], dtype=np.uint8)
+    bl, up = C.c_int(0), C.c_long(0)
+    err = _err()
+    rc = lib.ref_package_best(_ptr(a), a.shape[0], a.shape[1], ALG[alg], workers, _ptr(best), len(best),
+                              C.byref(bl), C.byref(up), err, 512)
+    _check(rc, err)
+    return dict(best=best[:bl.value].copy(), upper=int(up.value))
+
+
 # ----------------------------------------------------------------- C restatement (oracle/_build)
 
 

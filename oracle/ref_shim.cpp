@@ -20,6 +20,7 @@
 #include "symdist/distance.hpp"
 #include "symdist/engine.hpp"
 #include "symdist/errors.hpp"
+#include "symdist/gf4.hpp"
 #include "symdist/prep.hpp"
 
 using namespace symdist;
@@ -235,6 +236,68 @@ int ref_isometry_best(const uint8_t* bits, int rows, int cols, int workers, uint
         const StabilizerInstance inst = StabilizerInstance::from_matrix(from_bytes(bits, rows, cols));
         const std::vector<PackagedGamma> gammas = information_sets(isometry_transform(inst.a));
         const BoundsState st = run_bz(gammas, AdmissibilityFilter::for_rows(inst.a, inst.k), workers);
+        *upper = st.upper;
+        *best_len = static_cast<int>(st.best.size());
+        for (int i = 0; i < *best_len && i < best_cap; ++i) best[i] = st.best.get(static_cast<std::size_t>(i)) ? 1 : 0;
+    });
+}
+
+// The package routes' prep (alg 1: diagonalize_f2; 2: diagonalize_f4 + second_gamma): matrix j
+// as gamma_rows[j] x cols bytes at out + j*max_rows*cols; packages encoded per matrix as
+// [size, row...] runs (n_packages[j] of them).
+int ref_prepare_packages(const uint8_t* bits, int rows, int cols, int alg, int max_rows, uint8_t* out,
+                         int* gamma_rows, int* n_packages, int* n_pp, int* packages, int packages_cap,
+                         int* n_gammas, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const BitMatrix a = from_bytes(bits, rows, cols);
+        std::vector<PackagedGamma> gs;
+        if (alg == 1) {
+            gs.push_back(diagonalize_f2(a));
+        } else {
+            auto [b, pc] = diagonalize_f4(to_gf4(a));
+            PackagedGamma d = second_gamma(to_gf4(b.matrix), pc);
+            gs.push_back(std::move(b));
+            gs.push_back(std::move(d));
+        }
+        *n_gammas = static_cast<int>(gs.size());
+        int used = 0;
+        for (int j = 0; j < *n_gammas; ++j) {
+            const PackagedGamma& g = gs[static_cast<std::size_t>(j)];
+            if (static_cast<int>(g.matrix.n_rows()) > max_rows) throw std::invalid_argument("max_rows too small");
+            to_bytes(g.matrix, out + static_cast<std::size_t>(j) * max_rows * cols);
+            gamma_rows[j] = static_cast<int>(g.matrix.n_rows());
+            n_packages[j] = g.n_p();
+            n_pp[j] = g.n_pp;
+            for (const Package& pk : g.packages) {
+                if (used + 1 + static_cast<int>(pk.rows.size()) > packages_cap)
+                    throw std::invalid_argument("packages_cap too small");
+                packages[used++] = static_cast<int>(pk.rows.size());
+                for (int r : pk.rows) packages[used++] = r;
+            }
+        }
+    });
+}
+
+// saved_1_gamma / saved_2_gamma run through the reference's own prep and run_bz, returning the
+// bound state's best codeword (the single-worker BoundsState::best) and U.
+int ref_package_best(const uint8_t* bits, int rows, int cols, int alg, int workers, uint8_t* best,
+                     int best_cap, int* best_len, long* upper, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const StabilizerInstance inst = StabilizerInstance::from_matrix(from_bytes(bits, rows, cols));
+        std::vector<PackagedGamma> gs;
+        BitMatrix frame(0, inst.a.n_cols());
+        if (alg == 1) {
+            PackagedGamma g = diagonalize_f2(inst.a);
+            for (std::size_t r = 0; r < inst.a.n_rows(); ++r) frame.append_row(g.matrix.row(r));
+            gs.push_back(std::move(g));
+        } else {
+            auto [b, pc] = diagonalize_f4(to_gf4(inst.a));
+            PackagedGamma d = second_gamma(to_gf4(b.matrix), pc);
+            gs.push_back(std::move(b));
+            gs.push_back(std::move(d));
+            frame = inst.a;
+        }
+        const BoundsState st = run_bz(gs, AdmissibilityFilter::for_rows(std::move(frame), inst.k), workers);
         *upper = st.upper;
         *best_len = static_cast<int>(st.best.size());
         for (int i = 0; i < *best_len && i < best_cap; ++i) best[i] = st.best.get(static_cast<std::size_t>(i)) ? 1 : 0;

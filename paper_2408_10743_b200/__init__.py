@@ -10,6 +10,9 @@ this module                            reference
 ``RunOptions``                         ``RunOptions`` distance.hpp:33-37
 ``DistanceReport``                     ``DistanceReport`` distance.hpp:44-52
 ``saved_isometry``                     ``saved_isometry`` distance.cpp:135-149
+``saved_1_gamma`` / ``saved_2_gamma``  ``saved_1_gamma`` / ``saved_2_gamma`` distance.cpp:95-133
+``diagonalize_f2``                     ``diagonalize_f2`` prep.cpp:155-254
+``diagonalize_f4`` / ``second_gamma``  prep.cpp:256-297 (F4 package routes)
 ``compute_distance``                   ``compute_distance`` distance.cpp:226-240
 ``validate_normalizer``                ``validate_normalizer`` distance.cpp:71-93
 ``isometry_transform``                 ``isometry_transform`` prep.cpp:299-315
@@ -39,7 +42,8 @@ import numpy as np
 __all__ = [
     "Algorithm", "WeightMode", "StabilizerInstance", "RunOptions", "DistanceReport", "BoundsTraceEntry",
     "BoundsState", "PackagedGamma", "AdmissibilityFilter", "ValidationResult", "ParseError", "ValidationError",
-    "InternalError", "DeviceError", "saved_isometry", "compute_distance", "saved_isometry_batch", "run_bz",
+    "InternalError", "DeviceError", "saved_isometry", "saved_1_gamma", "saved_2_gamma", "compute_distance",
+    "diagonalize_f2", "prepare_packages", "saved_isometry_batch", "run_bz",
     "lower_bound", "validate_normalizer", "isometry_transform", "information_sets", "singleton_gamma",
     "generate_code", "Plan", "pack_rows", "unpack_rows", "library", "library_path", "device_available", "CONFIGS",
 ]
@@ -123,7 +127,7 @@ _EXPORTS = [
     "sdb_default_options", "sdb_last_error", "sdb_abi_version", "sdb_device_available", "sdb_saved_isometry",
     "sdb_compute_distance", "sdb_saved_isometry_batch", "sdb_run_bz", "sdb_lower_bound", "sdb_validate_normalizer",
     "sdb_isometry_transform", "sdb_information_sets", "sdb_generate_code", "sdb_plan_create", "sdb_plan_run",
-    "sdb_plan_destroy",
+    "sdb_plan_destroy", "sdb_saved_1_gamma", "sdb_saved_2_gamma", "sdb_run_bz_packaged", "sdb_prepare_packages",
 ]
 
 
@@ -336,6 +340,66 @@ def saved_isometry(inst, opts: Optional[RunOptions] = None, return_best: bool = 
     return out
 
 
+def _package_route(fn_name: str, inst, opts: Optional[RunOptions], return_best: bool):
+    inst = _inst(inst)
+    opts = opts or RunOptions()
+    w = pack_rows(inst.a)
+    o, keep = opts._c()
+    rep = _Report()
+    tr = (_Trace * _TRACE_CAP)()
+    best = np.zeros(max(1, (2 * inst.n + 63) // 64), dtype=np.uint64)
+    rc = getattr(library(), fn_name)(_wptr(w), w.shape[0], inst.a.shape[1], w.shape[1], C.byref(o), C.byref(rep), tr,
+                                     _TRACE_CAP, _wptr(best) if return_best else None)
+    del keep
+    _raise(rc)
+    out = _report(rep, tr, _TRACE_CAP)
+    if return_best:
+        return out, unpack_rows(best.reshape(1, -1), 2 * inst.n)[0]
+    return out
+
+
+def saved_1_gamma(inst, opts: Optional[RunOptions] = None, return_best: bool = False):
+    """Saved_1_Gamma (distance.cpp:95-113): diagonalize_f2 packages, one matrix, L = g + 1."""
+    return _package_route("sdb_saved_1_gamma", inst, opts, return_best)
+
+
+def saved_2_gamma(inst, opts: Optional[RunOptions] = None, return_best: bool = False):
+    """Saved_2_Gamma (distance.cpp:115-133): two F4-diagonalized matrices, the 2-matrix bound."""
+    return _package_route("sdb_saved_2_gamma", inst, opts, return_best)
+
+
+def prepare_packages(inst, alg: Algorithm) -> list:
+    """The package routes' prepared matrices: diagonalize_f2 (saved_1_gamma) or
+    diagonalize_f4 + second_gamma (saved_2_gamma), as PackagedGamma objects."""
+    inst = _inst(inst)
+    w = pack_rows(inst.a)
+    rows, cols = inst.a.shape
+    max_rows, cap = 2 * rows + 2, 16 * rows + 16
+    ow = max(1, (cols + 63) // 64)
+    out = np.zeros((2 * max_rows, ow), dtype=np.uint64)
+    gr, npk, npp = (np.zeros(2, dtype=np.int32) for _ in range(3))
+    pk = np.zeros(cap, dtype=np.int32)
+    ng = C.c_int(0)
+    ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+    _raise(library().sdb_prepare_packages(_wptr(w), rows, cols, w.shape[1], int(alg), 2, max_rows, _wptr(out), ow,
+                                          ip(gr), ip(npk), ip(npp), ip(pk), cap, C.byref(ng)))
+    res, pos = [], 0
+    for j in range(ng.value):
+        pkgs = []
+        for _ in range(int(npk[j])):
+            sz = int(pk[pos])
+            pkgs.append([int(x) for x in pk[pos + 1:pos + 1 + sz]])
+            pos += 1 + sz
+        mat = unpack_rows(out[j * max_rows:j * max_rows + int(gr[j])], cols)
+        res.append(PackagedGamma(matrix=mat, mode=WeightMode.symplectic, pair_count=cols // 2, rank_deficit=0,
+                                 pivots=[], packages=pkgs, n_pp=int(npp[j])))
+    return res
+
+
+def diagonalize_f2(a) -> PackagedGamma:
+    return prepare_packages(a, Algorithm.saved_1_gamma)[0]
+
+
 def compute_distance(inst, alg: Algorithm = Algorithm.saved_isometry, opts: Optional[RunOptions] = None):
     inst = _inst(inst)
     opts = opts or RunOptions()
@@ -425,15 +489,18 @@ def isometry_transform(a) -> np.ndarray:
 
 @dataclass
 class PackagedGamma:
-    """Singleton-package generator matrix (prep.hpp:25-35): packages[i] = {pivots[i], {i}}."""
+    """Generator matrix with its package partition (prep.hpp:25-35). packages = [] means every
+    row is its own package (singleton_gamma / information_sets)."""
     matrix: np.ndarray
     mode: WeightMode = WeightMode.hamming
     pair_count: int = 0
     rank_deficit: int = 0
     pivots: list = field(default_factory=list)
+    packages: list = field(default_factory=list)
+    n_pp: int = -1
 
     def n_p(self) -> int:
-        return int(self.matrix.shape[0])
+        return len(self.packages) if self.packages else int(self.matrix.shape[0])
 
 
 def singleton_gamma(m, mode: WeightMode) -> PackagedGamma:
@@ -499,7 +566,7 @@ def lower_bound(g: int, gammas: Sequence[PackagedGamma]) -> int:
         raise ValueError("lower_bound: no generator matrices")
     defs = np.array([gm.rank_deficit for gm in gammas], dtype=np.int32)
     nps = np.array([gm.n_p() for gm in gammas], dtype=np.int32)
-    npp = np.array([gm.n_p() for gm in gammas], dtype=np.int32)
+    npp = np.array([gm.n_pp if gm.n_pp >= 0 else gm.n_p() for gm in gammas], dtype=np.int32)
     out = C.c_longlong(0)
     ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
     _raise(library().sdb_lower_bound(g, int(gammas[0].mode), len(gammas), ip(defs), ip(nps), ip(npp), C.byref(out)))
@@ -514,6 +581,8 @@ def run_bz(gammas: Sequence[PackagedGamma], filt: AdmissibilityFilter, workers: 
     opts = opts or RunOptions(workers=workers)
     g0 = gammas[0]
     rows, cols = g0.matrix.shape
+    if any(gm.packages for gm in gammas) or len({gm.matrix.shape[0] for gm in gammas}) > 1:
+        return _run_bz_packaged(gammas, filt, opts)
     for gm in gammas:
         if gm.matrix.shape[1] != cols or gm.mode != g0.mode or gm.pair_count != g0.pair_count:
             raise ValueError("run_bz: generator matrices must share one codeword frame")
@@ -537,6 +606,54 @@ def run_bz(gammas: Sequence[PackagedGamma], filt: AdmissibilityFilter, workers: 
     rc = library().sdb_run_bz(_wptr(packed), len(gammas), rows, cols, words, int(g0.mode), g0.pair_count,
                               defs.ctypes.data_as(C.POINTER(C.c_int)), _wptr(fw), fr, fc, fwords, int(filt.enabled),
                               filt.k if filt.enabled else 0, C.byref(o), C.byref(rep), tr, _TRACE_CAP, _wptr(best))
+    del keep
+    _raise(rc)
+    r = _report(rep, tr, _TRACE_CAP)
+    lower = r.bounds_trace[-1].lower if r.bounds_trace else 1
+    return BoundsState(lower=lower, upper=r.upper, generation=r.generations,
+                       candidates_enumerated=r.candidates_enumerated, trace=r.trace_tuples(),
+                       best=unpack_rows(best.reshape(1, -1), cols)[0] if r.best_generation > 0 else np.zeros(0, np.uint8),
+                       report=r)
+
+
+def _run_bz_packaged(gammas, filt, opts):
+    g0 = gammas[0]
+    cols = g0.matrix.shape[1]
+    for gm in gammas:
+        if gm.matrix.shape[1] != cols or gm.mode != g0.mode or gm.pair_count != g0.pair_count:
+            raise ValueError("run_bz: generator matrices must share one codeword frame")
+        if gm.n_p() == 0:
+            raise ValueError("run_bz: matrix with no packages")
+    words = max(1, (cols + 63) // 64)
+    max_rows = max(gm.matrix.shape[0] for gm in gammas)
+    packed = np.zeros((len(gammas) * max_rows, words), dtype=np.uint64)
+    enc, npk = [], []
+    for j, gm in enumerate(gammas):
+        packed[j * max_rows:j * max_rows + gm.matrix.shape[0]] = pack_rows(gm.matrix)
+        pk = gm.packages or [[r] for r in range(gm.matrix.shape[0])]
+        npk.append(len(pk))
+        for p in pk:
+            enc += [len(p)] + list(p)
+    gr = np.array([gm.matrix.shape[0] for gm in gammas], dtype=np.int32)
+    npk = np.array(npk, dtype=np.int32)
+    npp = np.array([gm.n_pp for gm in gammas], dtype=np.int32)
+    defs = np.array([gm.rank_deficit for gm in gammas], dtype=np.int32)
+    enc = np.array(enc, dtype=np.int32)
+    if filt.normalizer is not None and filt.enabled:
+        fw = pack_rows(filt.normalizer)
+        fr, fc, fwords = filt.normalizer.shape[0], filt.normalizer.shape[1], fw.shape[1]
+    else:
+        fw = np.zeros((1, 1), dtype=np.uint64)
+        fr, fc, fwords = 0, 0, 1
+    o, keep = opts._c()
+    rep = _Report()
+    tr = (_Trace * _TRACE_CAP)()
+    best = np.zeros(words, dtype=np.uint64)
+    ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+    rc = library().sdb_run_bz_packaged(_wptr(packed), len(gammas), ip(gr), max_rows, cols, words, int(g0.mode),
+                                       g0.pair_count, ip(defs), ip(npk), ip(npp), ip(enc), _wptr(fw), fr, fc, fwords,
+                                       int(filt.enabled), filt.k if filt.enabled else 0, C.byref(o), C.byref(rep), tr,
+                                       _TRACE_CAP, _wptr(best))
     del keep
     _raise(rc)
     r = _report(rep, tr, _TRACE_CAP)

@@ -11,6 +11,7 @@
 #include "engine.hpp"
 #include "errors.hpp"
 #include "gf2.hpp"
+#include "packages.hpp"
 
 namespace {
 
@@ -98,6 +99,67 @@ void saved_isometry_impl(const uint64_t *rows, int n_rows, int n_cols, int row_w
     rep->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+sdb::GammaIn to_gamma_in(sdb::Packaged &&p) {
+    sdb::GammaIn g;
+    g.matrix = std::move(p.matrix);
+    g.rank_deficit = p.rank_deficit;
+    g.packages = std::move(p.packages);
+    g.n_pp = p.n_pp;
+    return g;
+}
+
+// The package routes' prep (reference distance.cpp:95-133): Saved_1_Gamma diagonalizes over
+// F2 and filters in the permuted frame (the first n+k prepared rows); Saved_2_Gamma runs the
+// two F4 diagonalizations and filters in the input frame.
+std::vector<sdb::GammaIn> package_gammas(const sdb::BitMat &a, int algorithm, sdb::BitMat *frame) {
+    std::vector<sdb::GammaIn> gammas;
+    if (algorithm == SDB_ALG_SAVED_1_GAMMA) {
+        sdb::Packaged pg = sdb::diagonalize_f2(a);
+        *frame = sdb::BitMat(a.rows, pg.matrix.cols);
+        for (int r = 0; r < a.rows; r++) std::copy(pg.matrix.row(r), pg.matrix.row(r) + pg.matrix.stride, frame->row(r));
+        gammas.push_back(to_gamma_in(std::move(pg)));
+    } else {
+        auto bp = sdb::diagonalize_f4(sdb::to_gf4(a));
+        sdb::Packaged d = sdb::second_gamma(sdb::to_gf4(bp.first.matrix), bp.second);
+        gammas.push_back(to_gamma_in(std::move(bp.first)));
+        gammas.push_back(to_gamma_in(std::move(d)));
+        *frame = a;
+    }
+    return gammas;
+}
+
+// saved_1_gamma / saved_2_gamma (distance.cpp:95-133): validate -> packages -> run_bz in
+// symplectic mode -> distance = U
+void package_route_impl(int algorithm, const uint64_t *rows, int n_rows, int n_cols, int row_words,
+                        const sdb_run_options &o, sdb_report *rep, sdb_trace_entry *trace, int trace_cap,
+                        uint64_t *best_out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_matrix_args(rows, n_rows, n_cols, row_words);
+    if (n_cols == 0 || n_cols % 2 != 0)
+        throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+    zero_report(rep);
+    const sdb::BitMat a = sdb::BitMat::from_words(rows, n_rows, n_cols, row_words);
+    const int n = n_cols / 2, k = n_rows - n;
+    if (o.validate) {
+        const sdb::Validation v = sdb::validate_normalizer(a);
+        if (!v.ok) throw sdb::ValidationFailure(v.message);
+    }
+    sdb::BitMat frame;
+    std::vector<sdb::GammaIn> gammas = package_gammas(a, algorithm, &frame);
+    sdb::Filter f;
+    f.enabled = o.dual_filter && k >= 1;
+    if (f.enabled) f.rows = std::move(frame);
+    const auto tp = std::chrono::steady_clock::now();
+    sdb::Plan plan(std::move(gammas), sdb::Mode::symplectic, n, f, o);
+    rep->h2d_bytes = plan.upload_bytes;
+    plan.run(rep, trace, trace_cap, best_out, nullptr);
+    rep->prep_seconds = std::chrono::duration<double>(tp - t0).count() + plan.h2d_seconds;
+    rep->distance = int(rep->upper);
+    rep->algorithm = algorithm;
+    rep->workers = o.workers;
+    rep->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 }  // namespace
 
 struct sdb_plan {
@@ -145,29 +207,84 @@ sdb_status sdb_saved_isometry(const uint64_t *rows, int n_rows, int n_cols, int 
     });
 }
 
+sdb_status sdb_saved_1_gamma(const uint64_t *rows, int n_rows, int n_cols, int row_words, const sdb_run_options *opts,
+                             sdb_report *report, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out) {
+    return guarded([&] {
+        if (!report) throw sdb::InvalidArgument("null report");
+        package_route_impl(SDB_ALG_SAVED_1_GAMMA, rows, n_rows, n_cols, row_words, opts_or_default(opts), report,
+                           trace, trace_cap, best_out);
+    });
+}
+
+sdb_status sdb_saved_2_gamma(const uint64_t *rows, int n_rows, int n_cols, int row_words, const sdb_run_options *opts,
+                             sdb_report *report, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out) {
+    return guarded([&] {
+        if (!report) throw sdb::InvalidArgument("null report");
+        package_route_impl(SDB_ALG_SAVED_2_GAMMA, rows, n_rows, n_cols, row_words, opts_or_default(opts), report,
+                           trace, trace_cap, best_out);
+    });
+}
+
+sdb_status sdb_prepare_packages(const uint64_t *rows, int n_rows, int n_cols, int row_words, int algorithm,
+                                int max_gammas, int max_rows, uint64_t *out, int out_row_words, int *gamma_rows,
+                                int *n_packages, int *n_pp, int *packages, int packages_cap, int *n_gammas) {
+    return guarded([&] {
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        if (n_cols == 0 || n_cols % 2 != 0)
+            throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+        if (algorithm != SDB_ALG_SAVED_1_GAMMA && algorithm != SDB_ALG_SAVED_2_GAMMA)
+            throw sdb::InvalidArgument("prepare_packages: saved_1_gamma or saved_2_gamma");
+        if (out_row_words < (n_cols + 63) / 64) throw sdb::InvalidArgument("out_row_words too small");
+        const sdb::BitMat a = sdb::BitMat::from_words(rows, n_rows, n_cols, row_words);
+        sdb::BitMat frame;
+        const std::vector<sdb::GammaIn> gs = package_gammas(a, algorithm, &frame);
+        if (n_gammas) *n_gammas = int(gs.size());
+        int used = 0;
+        for (int j = 0; j < int(gs.size()) && j < max_gammas; j++) {
+            const sdb::GammaIn &g = gs[size_t(j)];
+            if (g.matrix.rows > max_rows) throw sdb::InvalidArgument("prepare_packages: max_rows too small");
+            g.matrix.to_words(out + size_t(j) * max_rows * out_row_words, out_row_words);
+            gamma_rows[j] = g.matrix.rows;
+            n_packages[j] = int(g.packages.size());
+            n_pp[j] = g.n_pp;
+            for (const std::vector<int> &pk : g.packages) {
+                if (used + 1 + int(pk.size()) > packages_cap) throw sdb::InvalidArgument("packages_cap too small");
+                packages[used++] = int(pk.size());
+                for (int r : pk) packages[used++] = r;
+            }
+        }
+    });
+}
+
 sdb_status sdb_compute_distance(const uint64_t *rows, int n_rows, int n_cols, int row_words, int algorithm,
                                 const sdb_run_options *opts, sdb_report *report, sdb_trace_entry *trace,
                                 int trace_cap) {
     return guarded([&] {
         if (!report) throw sdb::InvalidArgument("null report");
         const int k = n_rows - n_cols / 2;
+        const sdb_run_options o = opts_or_default(opts);
         switch (algorithm) {
             case SDB_ALG_SAVED_ISOMETRY:
-                break;
+                saved_isometry_impl(rows, n_rows, n_cols, row_words, o, report, trace, trace_cap, nullptr);
+                return;
             case SDB_ALG_AUTO:
-                // distance.cpp:233-237: auto sends k <= 2 to saved_2_gamma
-                if (k <= 2) throw sdb::InvalidArgument("compute_distance: auto selects saved_2_gamma for k <= 2, "
-                                                       "which this build does not provide yet");
-                break;
+                // distance.cpp:233-237: the two-matrix route when k <= 2, else the isometry
+                if (k <= 2) {
+                    package_route_impl(SDB_ALG_SAVED_2_GAMMA, rows, n_rows, n_cols, row_words, o, report, trace,
+                                       trace_cap, nullptr);
+                } else {
+                    saved_isometry_impl(rows, n_rows, n_cols, row_words, o, report, trace, trace_cap, nullptr);
+                }
+                return;
             case SDB_ALG_SAVED_1_GAMMA:
             case SDB_ALG_SAVED_2_GAMMA:
+                package_route_impl(algorithm, rows, n_rows, n_cols, row_words, o, report, trace, trace_cap, nullptr);
+                return;
             case SDB_ALG_BRUTE_FORCE:
                 throw sdb::InvalidArgument("compute_distance: algorithm not provided by this build yet");
             default:
                 throw sdb::InvalidArgument("compute_distance: unknown algorithm");
         }
-        saved_isometry_impl(rows, n_rows, n_cols, row_words, opts_or_default(opts), report, trace, trace_cap,
-                            nullptr);
     });
 }
 
@@ -205,6 +322,53 @@ sdb_status sdb_run_bz(const uint64_t *gammas, int n_gammas, int n_rows, int n_co
             gs.push_back(sdb::GammaIn{sdb::BitMat::from_words(gammas + size_t(j) * n_rows * row_words, n_rows, n_cols,
                                                               row_words),
                                       rank_deficits ? rank_deficits[j] : 0});
+        sdb::Filter f;
+        f.enabled = filter_enabled && filter_k >= 1;
+        if (f.enabled) {
+            check_matrix_args(filter_rows, filter_n_rows, filter_n_cols, filter_row_words);
+            f.rows = sdb::BitMat::from_words(filter_rows, filter_n_rows, filter_n_cols, filter_row_words);
+        }
+        const sdb_run_options o = opts_or_default(opts);
+        sdb::Plan plan(std::move(gs), mode == SDB_MODE_HAMMING ? sdb::Mode::hamming : sdb::Mode::symplectic,
+                       pair_count, f, o);
+        plan.run(report, trace, trace_cap, best_out, nullptr);
+        report->distance = int(report->upper);
+        report->workers = o.workers;
+        report->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+sdb_status sdb_run_bz_packaged(const uint64_t *gammas, int n_gammas, const int *gamma_rows, int max_rows, int n_cols,
+                               int row_words, int mode, int pair_count, const int *rank_deficits,
+                               const int *n_packages, const int *n_pp, const int *packages,
+                               const uint64_t *filter_rows, int filter_n_rows, int filter_n_cols,
+                               int filter_row_words, int filter_enabled, int filter_k, const sdb_run_options *opts,
+                               sdb_report *report, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!report || !gamma_rows || !n_packages || !packages) throw sdb::InvalidArgument("null argument");
+        if (n_gammas <= 0) throw sdb::InvalidArgument("run_bz: need at least one generator matrix");
+        if (mode != SDB_MODE_SYMPLECTIC && mode != SDB_MODE_HAMMING) throw sdb::InvalidArgument("unknown weight mode");
+        check_matrix_args(gammas, max_rows * n_gammas, n_cols, row_words);
+        zero_report(report);
+        std::vector<sdb::GammaIn> gs;
+        int pos = 0;
+        for (int j = 0; j < n_gammas; j++) {
+            if (gamma_rows[j] < 0 || gamma_rows[j] > max_rows) throw sdb::InvalidArgument("gamma_rows out of range");
+            sdb::GammaIn g;
+            g.matrix = sdb::BitMat::from_words(gammas + size_t(j) * max_rows * row_words, gamma_rows[j], n_cols,
+                                               row_words);
+            g.rank_deficit = rank_deficits ? rank_deficits[j] : 0;
+            g.n_pp = n_pp ? n_pp[j] : -1;
+            for (int q = 0; q < n_packages[j]; q++) {
+                const int sz = packages[pos++];
+                if (sz < 1 || sz > 3) throw sdb::InvalidArgument("run_bz: packages hold one to three rows");
+                g.packages.emplace_back(packages + pos, packages + pos + sz);
+                pos += sz;
+            }
+            if (g.packages.empty()) throw sdb::InvalidArgument("run_bz: matrix with no packages");
+            gs.push_back(std::move(g));
+        }
         sdb::Filter f;
         f.enabled = filter_enabled && filter_k >= 1;
         if (f.enabled) {

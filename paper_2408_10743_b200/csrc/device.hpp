@@ -147,6 +147,33 @@ struct TilePlan {
 };
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms);
 
+// Package routes (Saved_1_Gamma / Saved_2_Gamma): a level-g
+// candidate picks g packages p_1 < ... < p_g and one member row of each; the reference
+// visits them in lexicographic order of (p_1, m_1, p_2, m_2, ...) (engine.cpp:202-219).
+// pkg_kernel<W> walks segments of that order: unrank through weighted suffix counts
+// wsuf(q, m) = number of m-package choices with members among packages [q, P), then the
+// lexicographic successor (next member of the deepest package that has one, else the next
+// package), one or a few row XORs per step.
+constexpr int kMaxPkgG = 4;
+struct PkgDev {
+    const short *pk_rows;              // [G][P][3] member rows, -1 padding
+    const unsigned char *pk_size;      // [G][P] members per package (1 or 3)
+    const unsigned long long *wsuf;    // [G][P + 1][BK]
+    int P;                             // package slots per Gamma (max over Gammas)
+    int np[kMaxPkgG];                  // packages of each Gamma
+};
+struct PkgLevel {
+    int g;
+    unsigned int thr0;
+    unsigned long long seg_len;
+    unsigned long long total[kMaxPkgG];  // candidates of each Gamma at this level
+    unsigned long long segs[kMaxPkgG];   // segments of each Gamma
+    unsigned long long seg_total;
+    int shard_rank, shard_world;
+};
+size_t pkg_smem_bytes(int G, int N, int W, int SW, int P, int BK);
+int launch_pkg_level(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, void *stream, int num_sms);
+
 // Batch: one code per CTA, the whole level loop on the device.
 struct BatchDev {
     const uint32_t *rows;      // [codes][G][N][2W]

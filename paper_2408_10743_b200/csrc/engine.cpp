@@ -90,12 +90,14 @@ void orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
 int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, std::vector<uint64_t> &out) {
     out.clear();
     if (!f.enabled) return 0;
-    const int G = int(gammas.size()), N = gammas[0].matrix.rows, F = f.rows.rows;
+    const int G = int(gammas.size()), F = f.rows.rows;
+    int N = 0;
+    for (const GammaIn &gm : gammas) N = std::max(N, gm.matrix.rows);
     // S: (G*N) x F, bit (i, r) = <first 2n columns of Gamma row i, filter row r>_s
     BitMat S(G * N, F);
     std::vector<uint64_t> proj(size_t((2 * n + 63) / 64));
     for (int j = 0; j < G; j++)
-        for (int i = 0; i < N; i++) {
+        for (int i = 0; i < gammas[size_t(j)].matrix.rows; i++) {
             std::fill(proj.begin(), proj.end(), 0);
             for (int c = 0; c < 2 * n; c++)
                 if (gammas[size_t(j)].matrix.get(i, c)) proj[size_t(c >> 6)] |= uint64_t(1) << (c & 63);
@@ -123,9 +125,30 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
     if (G_ > kMaxG) throw InvalidArgument("run_bz: too many generator matrices");
     N_ = gammas_[0].matrix.rows;
     const int cols = gammas_[0].matrix.cols;
-    for (const GammaIn &g : gammas_)
-        if (g.matrix.cols != cols || g.matrix.rows != N_)
-            throw InvalidArgument("run_bz: generator matrices must share one codeword frame");
+    for (const GammaIn &g : gammas_) {
+        if (!g.packages.empty()) packaged_ = true;
+        if (g.matrix.cols != cols) throw InvalidArgument("run_bz: generator matrices must share one codeword frame");
+        if (g.packages.empty() && g.matrix.rows == 0) throw InvalidArgument("run_bz: matrix with no packages");
+        N_ = std::max(N_, g.matrix.rows);
+    }
+    if (!packaged_)
+        for (const GammaIn &g : gammas_)
+            if (g.matrix.rows != N_) packaged_ = true;  // unequal package counts: packaged kernel
+    if (packaged_) {
+        if (G_ > kMaxPkgG) throw InvalidArgument("run_bz: package routes take at most 4 generator matrices");
+        for (GammaIn &g : gammas_) {
+            if (g.packages.empty())
+                for (int r = 0; r < g.matrix.rows; r++) g.packages.push_back({r});
+            if (g.packages.empty()) throw InvalidArgument("run_bz: matrix with no packages");
+            for (const std::vector<int> &pk : g.packages) {
+                if (pk.empty() || pk.size() > 3) throw InvalidArgument("run_bz: packages hold one to three rows");
+                for (int r : pk)
+                    if (r < 0 || r >= g.matrix.rows) throw InvalidArgument("run_bz: package row out of range");
+            }
+            np_.push_back(int(g.packages.size()));
+            P_ = std::max(P_, int(g.packages.size()));
+        }
+    }
     if (N_ == 0) throw InvalidArgument("run_bz: matrix with no packages");
     const int n = pair_count_;
     if (filter.enabled && filter.rows.cols != 2 * n)
@@ -163,7 +186,7 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
     if (W_ > kMaxW) throw InvalidArgument("rows too wide for the enumeration kernels (n > 256)");
     h_rows_.assign(size_t(G_) * N_ * 2 * W_, 0);
     for (int j = 0; j < G_; j++)
-        for (int r = 0; r < N_; r++) {
+        for (int r = 0; r < gammas_[size_t(j)].matrix.rows; r++) {
             uint32_t *dst = h_rows_.data() + (size_t(j) * N_ + r) * 2 * W_;
             const BitMat &m = gammas_[size_t(j)].matrix;
             if (image_layout_) {
@@ -173,10 +196,34 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
                 extract_bits(m, r, 0, cols, dst, W_);
             }
         }
-    orient_probe_words(h_rows_, G_, N_, W_);
+    if (!packaged_) orient_probe_words(h_rows_, G_, N_, W_);
     SW_ = build_syndromes(gammas_, n, filter, h_syn_);
     BK_ = std::min(N_, kMaxLevel) + 2;
     h_binom_ = binom_table(N_, BK_);
+    if (packaged_) {
+        // package tables and weighted suffix counts wsuf(q, m) = wsuf(q+1, m) + s_q wsuf(q+1, m-1)
+        const unsigned long long cap = 1ull << 62;
+        h_pk_rows_.assign(size_t(G_) * P_ * 3, -1);
+        h_pk_size_.assign(size_t(G_) * P_, 0);
+        h_wsuf_.assign(size_t(G_) * (P_ + 1) * BK_, 0);
+        for (int j = 0; j < G_; j++) {
+            const auto &pk = gammas_[size_t(j)].packages;
+            const int np = int(pk.size());
+            for (int q = 0; q < np; q++) {
+                h_pk_size_[size_t(j) * P_ + q] = (unsigned char)pk[size_t(q)].size();
+                for (size_t m = 0; m < pk[size_t(q)].size(); m++)
+                    h_pk_rows_[(size_t(j) * P_ + q) * 3 + m] = short(pk[size_t(q)][m]);
+            }
+            unsigned long long *ws = h_wsuf_.data() + size_t(j) * (P_ + 1) * BK_;
+            ws[size_t(np) * BK_] = 1;
+            for (int q = np - 1; q >= 0; q--)
+                for (int m = 0; m < BK_; m++) {
+                    const unsigned long long a = ws[size_t(q + 1) * BK_ + m],
+                                             b = m ? ws[size_t(q + 1) * BK_ + m - 1] * pk[size_t(q)].size() : 0;
+                    ws[size_t(q) * BK_ + m] = (a >= cap || b >= cap || a + b >= cap) ? cap : a + b;
+                }
+        }
+    }
     upload();
 }
 
@@ -276,7 +323,10 @@ void Plan::upload() {
                  b_state = align256(sizeof(LevelState) + size_t(max_weight_ + 1) * 8),
                  b_ctl = align256(sizeof(RunCtl)), b_trace = align256(size_t(N_ + 1) * 4),
                  b_counters = align256(size_t(N_ + 1) * 8), b_tables = align256(table_cap_ * 8);
-    d_bytes_ = b_rows + b_syn + b_binom + b_state + b_ctl + b_trace + 2 * b_counters + b_tables;
+    const size_t b_pkr = align256(h_pk_rows_.size() * 2 + 2), b_pks = align256(h_pk_size_.size() + 1),
+                 b_ws = align256(h_wsuf_.size() * 8 + 8);
+    d_bytes_ = b_rows + b_syn + b_binom + b_state + b_ctl + b_trace + 2 * b_counters + b_tables +
+               (packaged_ ? b_pkr + b_pks + b_ws : 0);
     const auto t0 = std::chrono::steady_clock::now();
     d_mem_ = workspace_get(device_, d_bytes_);
     unsigned char *base = static_cast<unsigned char *>(d_mem_);
@@ -304,6 +354,25 @@ void Plan::upload() {
     d_counter_init_ = reinterpret_cast<unsigned long long *>(q);
     q += b_counters;
     d_tables_ = reinterpret_cast<unsigned long long *>(q);
+    q += b_tables;
+    if (packaged_) {
+        pk_.pk_rows = reinterpret_cast<const short *>(q);
+        check_cuda(cudaMemcpyAsync(q, h_pk_rows_.data(), h_pk_rows_.size() * 2, cudaMemcpyHostToDevice, stream_),
+                   "H2D packages");
+        q += b_pkr;
+        pk_.pk_size = reinterpret_cast<const unsigned char *>(q);
+        check_cuda(cudaMemcpyAsync(q, h_pk_size_.data(), h_pk_size_.size(), cudaMemcpyHostToDevice, stream_),
+                   "H2D packages");
+        q += b_pks;
+        pk_.wsuf = reinterpret_cast<const unsigned long long *>(q);
+        check_cuda(cudaMemcpyAsync(q, h_wsuf_.data(), h_wsuf_.size() * 8, cudaMemcpyHostToDevice, stream_),
+                   "H2D packages");
+        pk_.P = P_;
+        for (int j = 0; j < G_; j++) pk_.np[j] = np_[size_t(j)];
+        upload_bytes += h_pk_rows_.size() * 2 + h_pk_size_.size() + h_wsuf_.size() * 8;
+        if (pkg_smem_bytes(G_, N_, W_, SW_, P_, BK_) > 200 * 1024)
+            throw InvalidArgument("problem too large for shared-memory staging");
+    }
     h_counter_init_.assign(size_t(N_ + 1), 0);
     check_cuda(cudaMemcpyAsync(d_counter_init_, h_counter_init_.data(), size_t(N_ + 1) * 8, cudaMemcpyHostToDevice,
                                stream_),
@@ -369,14 +438,51 @@ long long Plan::lower_bound(int g) const {
         return s;
     }
     if (G_ == 1) return (long long)g + 1;
-    if (G_ == 2) return (long long)g + 1 + std::max(0LL, (long long)g + 1);
+    if (G_ == 2) {
+        const GammaIn &d = gammas_[1];
+        const long long np = d.packages.empty() ? d.matrix.rows : (long long)d.packages.size();
+        const long long npp = d.n_pp < 0 ? np : d.n_pp;
+        return (long long)g + 1 + std::max(0LL, (long long)g + 1 + npp - np);
+    }
     throw InvalidArgument("lower_bound: symplectic mode takes one or two matrices");
+}
+
+unsigned long long Plan::level_candidates(int g) const {
+    if (!packaged_) return binom_u64(N_, g) * (unsigned long long)G_;
+    unsigned long long t = 0;
+    for (int j = 0; j < G_; j++) t += h_wsuf_[size_t(j) * (P_ + 1) * BK_ + size_t(g)];
+    return t;
 }
 
 void Plan::prepare_level(int g) {
     LevelHost &lv = levels_[size_t(g)];
     if (lv.ready) return;
     const int world = std::max(1, opts_.world), rank = opts_.rank;
+    if (packaged_) {
+        if (g >= BK_) throw InvalidArgument("generation beyond the kernels' combination-size limit");
+        PkgLevel &L = lv.pkg;
+        L.g = g;
+        L.thr0 = ~0u;
+        unsigned long long total = 0;
+        for (int j = 0; j < G_; j++) {
+            L.total[j] = h_wsuf_[size_t(j) * (P_ + 1) * BK_ + size_t(g)];
+            if (L.total[j] >= (1ull << kKeyRankBits))
+                throw InvalidArgument("level too large for 58-bit combination ranks");
+            total += L.total[j];
+        }
+        const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
+        L.seg_len = std::max<unsigned long long>(64, (total + threads_total * 4 - 1) / (threads_total * 4));
+        L.seg_total = 0;
+        for (int j = 0; j < G_; j++) {
+            L.segs[j] = (L.total[j] + L.seg_len - 1) / L.seg_len;
+            L.seg_total += L.segs[j];
+        }
+        L.shard_rank = rank;
+        L.shard_world = world;
+        lv.t = -1;
+        lv.ready = true;
+        return;
+    }
     const unsigned long long per = binom_u64(N_, g);
     if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
     const unsigned long long total = per * (unsigned long long)G_;
@@ -445,7 +551,10 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     const int world = std::max(1, opts_.world), rank = opts_.rank;
     if (rank < 0 || rank >= world) throw InvalidArgument("rank outside [0, world)");
     if (world > 1 && !opts_.allreduce_min) throw InvalidArgument("world > 1 needs an allreduce_min callback");
+    // every matrix generates the full code: the smallest package count closes the search
+    // (engine.cpp:322-325)
     int g_limit = N_;
+    if (packaged_) g_limit = *std::min_element(np_.begin(), np_.end());
     if (opts_.max_generation > 0) g_limit = std::min(g_limit, opts_.max_generation);
     if (g_limit > kMaxLevel) g_limit = kMaxLevel;  // checked again below if the run gets there
     constexpr unsigned long long kSyncCandidates = 1ull << 28;  // ~0.1 ms of kernel time
@@ -459,8 +568,9 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         prepare_level(g);
         const LevelHost &lv = levels_[size_t(g)];
         check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
-        const int nl = lv.t == 0 ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
-                                 : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
+        const int nl = lv.t < 0    ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
+                       : lv.t == 0 ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
+                                   : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
         if (nl < 0) throw InvalidArgument("unsupported row width");
         launches += nl;
         check_cuda(cudaGetLastError(), "level kernel launch");
@@ -496,14 +606,14 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         check_cuda(cudaGetLastError(), "level close launch");
         check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
         last_g = g;
-        const unsigned long long total = binom_u64(N_, g) * (unsigned long long)G_;
+        const unsigned long long total = level_candidates(g);
         if (world > 1 || total >= kSyncCandidates || g == g_limit) {
             check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
             check_cuda(cudaStreamSynchronize(stream_), "level sync");
             d2h += sizeof ctl;
             if (ctl.done) break;
         }
-        if (g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
+        if (!packaged_ && g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
             throw InvalidArgument("generation beyond the kernels' combination-size limit");
     }
     std::vector<int> tu(size_t(last_g + 1));
@@ -524,13 +634,13 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         float ms = 0;
         check_cuda(cudaEventElapsedTime(&ms, level_event(2 * g), level_event(2 * g + 1)), "event time");
         enum_s += ms * 1e-3;
-        candidates += binom_u64(N_, g) * (unsigned long long)G_;
+        candidates += level_candidates(g);
         generation = g;
         if (n_levels < trace_cap && trace) trace[n_levels] = sdb_trace_entry{g, L, U};
         if (level_seconds && n_levels < trace_cap) level_seconds[n_levels] = ms * 1e-3;
         n_levels++;
         if (L >= U) { complete = true; break; }
-        if (g == N_) complete = true;
+        if (g == (packaged_ ? *std::min_element(np_.begin(), np_.end()) : N_)) complete = true;
     }
     if (complete && U >= sentinel_)
         throw InternalFailure("run_bz: no admissible codeword after complete enumeration; "
@@ -555,21 +665,44 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     if (best_out) {
         const BitMat &m = gammas_[size_t(std::max(0, best_j))].matrix;
         std::vector<uint64_t> acc(size_t(m.stride), 0);
-        if (best_g > 0) {
-            // lexicographic unrank (host twin of the kernels' unrank_lex)
-            unsigned long long r = best_r;
-            int v = 0;
-            for (int i = 0; i < best_g; i++) {
-                for (;; v++) {
-                    const unsigned long long cnt = binom_u64(N_ - 1 - v, best_g - 1 - i);
-                    if (r < cnt) break;
-                    r -= cnt;
-                }
-                for (int w = 0; w < m.stride; w++) acc[size_t(w)] ^= m.row(v)[w];
-                v++;
-            }
-        }
+        if (best_g > 0) unrank_best(best_g, best_j, best_r, acc);
         std::copy(acc.begin(), acc.end(), best_out);
+    }
+}
+
+// Host twin of the kernels' unranking: the codeword at lexicographic rank r of level g of
+// Gamma j, in the reference's visiting order (engine.cpp:202-219).
+void Plan::unrank_best(int g, int j, unsigned long long r, std::vector<uint64_t> &acc) const {
+    const BitMat &m = gammas_[size_t(j)].matrix;
+    if (!packaged_) {
+        int v = 0;
+        for (int i = 0; i < g; i++) {
+            for (;; v++) {
+                const unsigned long long cnt = binom_u64(N_ - 1 - v, g - 1 - i);
+                if (r < cnt) break;
+                r -= cnt;
+            }
+            for (int w = 0; w < m.stride; w++) acc[size_t(w)] ^= m.row(v)[w];
+            v++;
+        }
+        return;
+    }
+    const auto &pk = gammas_[size_t(j)].packages;
+    const unsigned long long *ws = h_wsuf_.data() + size_t(j) * (P_ + 1) * BK_;
+    int q = 0;
+    for (int i = 0; i < g; i++) {
+        for (;; q++) {
+            const unsigned long long sub = ws[size_t(q + 1) * BK_ + size_t(g - 1 - i)];
+            const unsigned long long cnt = pk[size_t(q)].size() * sub;
+            if (r < cnt) {
+                const int row = pk[size_t(q)][size_t(r / sub)];
+                r %= sub;
+                for (int w = 0; w < m.stride; w++) acc[size_t(w)] ^= m.row(row)[w];
+                break;
+            }
+            r -= cnt;
+        }
+        q++;
     }
 }
 

@@ -20,6 +20,10 @@ enum class Mode { symplectic = 0, hamming = 1 };
 struct GammaIn {
     BitMat matrix;
     int rank_deficit = 0;
+    // package routes: member rows of each package (1 or 3 rows); empty = every row is its
+    // own package, in row order. n_pp: packages pivoted on principal columns (-1: all)
+    std::vector<std::vector<int>> packages;
+    int n_pp = -1;
 };
 
 struct Filter {
@@ -60,6 +64,7 @@ class Plan {
         int t = 0;                    // 0: walk kernel, else the tile kernel's tail size
         LevelLaunch walk{};
         TilePlan tile{};
+        PkgLevel pkg{};
     };
 
     void upload();
@@ -88,6 +93,16 @@ class Plan {
     unsigned long long *d_tables_ = nullptr;    // tile unit tables of all levels, back to back
     size_t table_cap_ = 0, table_used_ = 0;
     std::vector<unsigned long long> h_counter_init_, h_table_;
+    // package routes
+    bool packaged_ = false;
+    int P_ = 0;                                  // package slots per Gamma
+    std::vector<int> np_;                        // packages of each Gamma
+    std::vector<short> h_pk_rows_;               // [G][P][3]
+    std::vector<unsigned char> h_pk_size_;       // [G][P]
+    std::vector<unsigned long long> h_wsuf_;     // [G][P + 1][BK]
+    PkgDev pk_{};
+    unsigned long long level_candidates(int g) const;
+    void unrank_best(int g, int j, unsigned long long r, std::vector<uint64_t> &acc) const;
 };
 
 // Host cost model for one level: 0 = lexicographic-walk kernel, else the tail size t of

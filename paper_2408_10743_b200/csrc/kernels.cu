@@ -173,6 +173,139 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
     if ((threadIdx.x & 31) == 0 && visited) atomicAdd(&p.state->visited, visited);
 }
 
+// ---------------------------------------------------------------- packages (1/3-packages)
+
+__host__ __device__ size_t pkg_layout(int G, int N, int W, int SW, int P, int BK, size_t *o_syn, size_t *o_pr, size_t *o_ps,
+                                      size_t *o_ws) {
+    size_t off = ((size_t(G) * N * 2 * W * 4) + 15) & ~size_t(15);
+    *o_syn = off;
+    off += size_t(G) * N * SW * 8;
+    *o_pr = off;
+    off += ((size_t(G) * P * 3 * 2) + 15) & ~size_t(15);
+    *o_ps = off;
+    off += ((size_t(G) * P) + 15) & ~size_t(15);
+    *o_ws = off;
+    off += size_t(G) * (P + 1) * BK * 8;
+    return off;
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) pkg_kernel(ProblemDev p, PkgDev k, PkgLevel L) {
+    if (run_done(p)) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int rowlen = 2 * W, G = p.G, N = p.N, SW = p.SW, P = k.P, BK = p.BK;
+    size_t o_syn, o_pr, o_ps, o_ws;
+    pkg_layout(G, N, W, SW, P, BK, &o_syn, &o_pr, &o_ps, &o_ws);
+    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem);
+    unsigned long long *s_syn = reinterpret_cast<unsigned long long *>(smem + o_syn);
+    short *s_pr = reinterpret_cast<short *>(smem + o_pr);
+    unsigned char *s_ps = smem + o_ps;
+    unsigned long long *s_ws = reinterpret_cast<unsigned long long *>(smem + o_ws);
+    for (int i = threadIdx.x; i < G * N * rowlen; i += blockDim.x) s_rows[i] = p.rows[i];
+    for (int i = threadIdx.x; i < G * N * SW; i += blockDim.x) s_syn[i] = p.syn[i];
+    for (int i = threadIdx.x; i < G * P * 3; i += blockDim.x) s_pr[i] = k.pk_rows[i];
+    for (int i = threadIdx.x; i < G * P; i += blockDim.x) s_ps[i] = k.pk_size[i];
+    for (int i = threadIdx.x; i < G * (P + 1) * BK; i += blockDim.x) s_ws[i] = k.wsuf[i];
+    __syncthreads();
+
+    const int g = L.g;
+    unsigned thr = start_threshold(p, L.thr0);
+    unsigned long long visited = 0;
+    int pk[kMaxLevel], d[kMaxLevel];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long it = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;; it += stride) {
+        unsigned long long seg = it * L.shard_world + L.shard_rank;
+        if (seg >= L.seg_total) break;
+        int j = 0;
+        while (seg >= L.segs[j]) seg -= L.segs[j++];
+        const int np = k.np[j];
+        const unsigned long long r0 = seg * L.seg_len, r1 = min(r0 + L.seg_len, L.total[j]);
+        const uint32_t *grows = s_rows + j * N * rowlen;
+        const unsigned long long *gsyn = s_syn + j * N * SW;
+        const short *prow = s_pr + j * P * 3;
+        const unsigned char *psz = s_ps + j * P;
+        const unsigned long long *ws = s_ws + size_t(j) * (P + 1) * BK;  // ws[q * BK + m]
+        // unrank r0 in the reference's order: (package, member) pairs, lexicographic
+        uint32_t acc[2 * W];
+#pragma unroll
+        for (int i = 0; i < 2 * W; i++) acc[i] = 0;
+        {
+            unsigned long long rho = r0;
+            int q = 0;
+            for (int i = 0; i < g; i++) {
+                for (;; q++) {
+                    const unsigned long long sub = ws[(q + 1) * BK + (g - 1 - i)];
+                    const unsigned long long cnt = psz[q] * sub;
+                    if (rho < cnt) {
+                        pk[i] = q;
+                        d[i] = int(rho / sub);
+                        rho %= sub;
+                        break;
+                    }
+                    rho -= cnt;
+                }
+                xor_row<W>(acc, grows + prow[q * 3 + d[i]] * rowlen);
+                q++;
+            }
+        }
+        unsigned long long r = r0;
+        for (;;) {
+            const unsigned w = unsigned(p.scale * weight_of<W>(acc));
+            if (w <= thr) {
+                bool adm = SW == 0;
+                for (int s = 0; s < SW && !adm; s++) {
+                    unsigned long long x = 0;
+                    for (int i = 0; i < g; i++) x ^= gsyn[prow[pk[i] * 3 + d[i]] * SW + s];
+                    adm = x != 0;
+                }
+                if (adm) {
+                    atomicMin(&p.state->wmin, w);
+                    atomicMin(&p.key_by_w[w], ((unsigned long long)j << kKeyRankBits) | r);
+                    thr = w;
+                }
+            }
+            if (++r >= r1) break;
+            // successor: the deepest position that can take its next member or next package
+            int i = g - 1;
+            while (d[i] + 1 >= psz[pk[i]] && pk[i] + 1 > np - (g - i)) i--;
+            for (int m = i; m < g; m++) xor_row<W>(acc, grows + prow[pk[m] * 3 + d[m]] * rowlen);
+            if (d[i] + 1 < psz[pk[i]]) {
+                d[i]++;
+            } else {
+                pk[i]++;
+                d[i] = 0;
+            }
+            for (int m = i + 1; m < g; m++) {
+                pk[m] = pk[m - 1] + 1;
+                d[m] = 0;
+            }
+            for (int m = i; m < g; m++) xor_row<W>(acc, grows + prow[pk[m] * 3 + d[m]] * rowlen);
+        }
+        visited += r1 - r0;
+        thr = min(thr, *(volatile unsigned int *)&p.state->wmin);
+    }
+    for (int o = 16; o > 0; o >>= 1) visited += __shfl_down_sync(0xffffffffu, visited, o);
+    if ((threadIdx.x & 31) == 0 && visited) atomicAdd(&p.state->visited, visited);
+}
+
+template <int W>
+int launch_pkg_impl(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, cudaStream_t st, int num_sms) {
+    size_t a, b, c, d;
+    const size_t smem = pkg_layout(p.G, p.N, W, p.SW, k.P, p.BK, &a, &b, &c, &d);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(pkg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    const unsigned long long segs = (L.seg_total + L.shard_world - 1 - L.shard_rank) / L.shard_world;
+    unsigned long long blocks = (segs + 255) / 256;
+    const unsigned long long cap = (unsigned long long)num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) return 0;
+    pkg_kernel<W><<<unsigned(blocks), 256, smem, st>>>(p, k, L);
+    return 1;
+}
+
 // ---------------------------------------------------------------- batch: one code per CTA
 
 template <int W>
@@ -638,6 +771,26 @@ int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, i
         case 6: return launch_walk_impl<6>(p, L, st, num_sms);
         case 7: return launch_walk_impl<7>(p, L, st, num_sms);
         case 8: return launch_walk_impl<8>(p, L, st, num_sms);
+    }
+    return -1;
+}
+
+size_t pkg_smem_bytes(int G, int N, int W, int SW, int P, int BK) {
+    size_t a, b, c, d;
+    return pkg_layout(G, N, W, SW, P, BK, &a, &b, &c, &d);
+}
+
+int launch_pkg_level(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, void *stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (p.W) {
+        case 1: return launch_pkg_impl<1>(p, k, L, st, num_sms);
+        case 2: return launch_pkg_impl<2>(p, k, L, st, num_sms);
+        case 3: return launch_pkg_impl<3>(p, k, L, st, num_sms);
+        case 4: return launch_pkg_impl<4>(p, k, L, st, num_sms);
+        case 5: return launch_pkg_impl<5>(p, k, L, st, num_sms);
+        case 6: return launch_pkg_impl<6>(p, k, L, st, num_sms);
+        case 7: return launch_pkg_impl<7>(p, k, L, st, num_sms);
+        case 8: return launch_pkg_impl<8>(p, k, L, st, num_sms);
     }
     return -1;
 }

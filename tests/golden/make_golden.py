@@ -158,6 +158,63 @@ def engine_kats() -> dict:
     return dict(cases=cases)
 
 
+def package_routes(heavy: bool, workers: int) -> dict:
+    """Saved_1_Gamma / Saved_2_Gamma answered by the reference:
+    BASELINE configs 1-2 (config 4 for 1-Gamma with --heavy), the reference tests' worked
+    examples, random instances with the brute-force distance, auto dispatch (k <= 2 sends
+    to saved_2_gamma, distance.cpp:233-237) and the first 256 config-3 codes."""
+    cases = []
+
+    def add(src, a, algs=("saved_1_gamma", "saved_2_gamma"), best=True, brute=False, validate=True, filt=True,
+            **extra):
+        for alg in algs:
+            r = O.ref_compute_distance(a, alg, workers=workers if a.shape[1] > 60 else 1, validate=validate,
+                                       dual_filter=filt)
+            case = dict(src=src, alg=alg, n=a.shape[1] // 2, k=a.shape[0] - a.shape[1] // 2, normalizer=hexrows(a),
+                        distance=r.distance, trace=r.trace, candidates=r.candidates, generations=r.generations,
+                        validate=validate, dual_filter=filt, **extra)
+            if best:
+                b = O.ref_package_best(a, alg)
+                case["best"] = hexrows([b["best"]])[0]
+                case["best_len"] = int(len(b["best"]))
+            if brute:
+                case["brute"] = O.ref_compute_distance(a, "brute_force").distance
+            cases.append(case)
+
+    for cid in (1, 2):
+        c = O.CONFIGS[cid]
+        add(f"config{cid}", O.generate(c["n"], c["k"], c["seed"]), config=cid)
+    if heavy:
+        c = O.CONFIGS[4]
+        add("config4", O.generate(c["n"], c["k"], c["seed"]), algs=("saved_1_gamma",), best=False, config=4)
+    # proj/tests/test_engine.cpp:205-219 / test_prep.cpp:14: the 3x4 example
+    add("test_prep.cpp:14", np.array([[1, 0, 0, 1], [0, 1, 1, 0], [0, 0, 1, 1]], dtype=np.uint8), brute=True)
+    # test_prep.cpp:17-19 additive example rows (1,1,1,1), (a,0,a,a), (0,a2,a2,a2) as (a | b)
+    add("test_prep.cpp:17-19", np.array([[int(ch) for ch in row] for row in
+                                         ("11110000", "00001011", "01110111")], dtype=np.uint8),
+        algs=("saved_2_gamma",), validate=False, filt=False)
+    for n in (2, 6):  # test_distance.cpp:57-64 style (I_n | 0)
+        ident = np.zeros((n, 2 * n), dtype=np.uint8)
+        for i in range(n):
+            ident[i, i] = 1
+        add("test_distance.cpp:57-64", ident, brute=True)
+    # test_distance.cpp:102-117 style: random instances against the brute-force oracle
+    for i in range(40):
+        n = 3 + i % 10
+        k = (7 * i) % (n + 1)
+        add("test_distance.cpp:102-117", O.ref_random_stabilizer(n, k, 20000 + 31 * i), brute=True, seed=20000 + 31 * i)
+    for n, k, seed in [(16, 1, 11), (18, 2, 12), (20, 0, 13), (22, 2, 14)]:  # test_distance.cpp:122-125
+        add("test_distance.cpp:122-125", O.ref_random_stabilizer(n, k, seed), seed=seed)
+    # auto dispatch on the first 256 config-3 codes (k = 2: saved_2_gamma)
+    c = O.CONFIGS[3]
+    batch = []
+    for s in c["seeds"][:256]:
+        a = O.generate(c["n"], c["k"], s)
+        r = O.ref_compute_distance(a, "auto")
+        batch.append(dict(seed=s, alg=r.algorithm, distance=r.distance, trace=r.trace, candidates=r.candidates))
+    return dict(cases=cases, config3_auto=dict(n=c["n"], k=c["k"], codes=batch))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true", help="also config 4 (full) and config 5 (g<=8)")
@@ -179,6 +236,8 @@ def main() -> None:
         dump("reference_kats.json", reference_kats())
     if want("engine"):
         dump("engine_kats.json", engine_kats())
+    if want("packages"):
+        dump("package_routes.json", package_routes(args.heavy, args.workers))
     if args.heavy and want("c4"):
         dump("config4.json", single_config(4, args.workers))
     if args.heavy and want("c5"):

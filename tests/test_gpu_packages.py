@@ -1,0 +1,112 @@
+"""GPU parity of the package routes (Saved_1_Gamma / Saved_2_Gamma)
+against the reference's own answers (tests/golden/package_routes.json, make_golden.py):
+distance, the (g, L, U) trace, candidates_enumerated and the best codeword (the
+single-worker BoundsState::best), through the C ABI."""
+import numpy as np
+import pytest
+
+from conftest import hex_to_mat, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def tr(rep):
+    return [e.astuple() for e in rep.bounds_trace]
+
+
+def _run(gpu, case, kernel=0, **kw):
+    a = hex_to_mat(case["normalizer"], 2 * case["n"])
+    o = gpu.RunOptions(validate=case.get("validate", True), dual_filter=case.get("dual_filter", True), **kw)
+    fn = gpu.saved_1_gamma if case["alg"] == "saved_1_gamma" else gpu.saved_2_gamma
+    return fn(a, o, return_best=True)
+
+
+
+
+@pytest.mark.parametrize("which", ["configs", "examples", "random"])
+def test_package_routes_bit_exact(gpu, which):
+    gd = load_golden("package_routes.json")
+    sel = {"configs": lambda c: c["src"].startswith("config"),
+           "examples": lambda c: c["src"].startswith("test_prep") or c["src"].startswith("test_distance.cpp:57"),
+           "random": lambda c: c["src"].startswith("test_distance.cpp:1")}[which]
+    cases = [c for c in gd["cases"] if sel(c)]
+    assert cases
+    for case in cases:
+        rep, best = _run(gpu, case)
+        assert rep.distance == case["distance"], case["src"]
+        assert tr(rep) == [tuple(t) for t in case["trace"]], (case["src"], case["alg"])
+        assert rep.candidates_enumerated == case["candidates"]
+        assert rep.candidates_visited == case["candidates"]
+        assert rep.generations == case["generations"]
+        if "best" in case:
+            assert (best == hex_to_mat([case["best"]], case["best_len"])[0]).all(), (case["src"], case["alg"])
+        if "brute" in case:
+            assert rep.distance == case["brute"]
+
+
+def test_auto_dispatch_sends_small_k_to_two_gamma(gpu):
+    gd = load_golden("package_routes.json")["config3_auto"]
+    for c in gd["codes"][:64]:
+        a = gpu.generate_code(gd["n"], gd["k"], c["seed"])
+        rep = gpu.compute_distance(a, gpu.Algorithm.auto_select)
+        assert rep.algorithm == gpu.Algorithm.saved_2_gamma
+        assert rep.distance == c["distance"]
+        assert tr(rep) == [tuple(t) for t in c["trace"]]
+        assert rep.candidates_enumerated == c["candidates"]
+
+
+def test_run_bz_with_prepared_packages(gpu):
+    # the engine seam (engine.hpp:60-61) with the routes' prepared matrices, and the additive
+    # example of test_engine.cpp:184-203: bounds (1, 2, 3), (2, 3, 2), best = (a2, a, 0, 0)
+    add = np.array([[int(ch) for ch in r] for r in ("11110000", "00001011", "01110111")], dtype=np.uint8)
+    b, _ = gpu.prepare_packages(add, gpu.Algorithm.saved_2_gamma)
+    st = gpu.run_bz([b], gpu.AdmissibilityFilter.disabled())
+    assert st.trace == [(1, 2, 3), (2, 3, 2)]
+    assert st.upper == 2
+    assert st.best.tolist() == [int(ch) for ch in "10001100"]
+    naive = gpu.run_bz([gpu.singleton_gamma(add, gpu.WeightMode.symplectic)], gpu.AdmissibilityFilter.disabled())
+    assert naive.upper == 3
+    # test_engine.cpp:205-219: the 3x4 example through diagonalize_f2
+    ex = np.array([[1, 0, 0, 1], [0, 1, 1, 0], [0, 0, 1, 1]], dtype=np.uint8)
+    g = gpu.diagonalize_f2(ex)
+    st = gpu.run_bz([g], gpu.AdmissibilityFilter.for_rows(g.matrix[:3], 1))
+    assert st.upper == 1 and st.generation == 1 and st.candidates_enumerated == 4
+    # sharded packaged levels merge to the single-rank answer
+    c = gpu.CONFIGS[2]
+    a = gpu.generate_code(c["n"], c["k"], c["seed"])
+    one = gpu.saved_2_gamma(a)
+    import threading
+
+    vals, barrier = {}, threading.Barrier(2)
+
+    def fn_for(r):
+        def fn(v):
+            vals[r] = v.copy()
+            barrier.wait()
+            out = np.minimum(vals[0], vals[1])
+            barrier.wait()
+            return out
+        return fn
+
+    out = [None, None]
+
+    def run(r):
+        out[r] = gpu.saved_2_gamma(a, gpu.RunOptions(rank=r, world=2, allreduce_min=fn_for(r)))
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for rep in out:
+        assert tr(rep) == tr(one) and rep.distance == one.distance == 7
+    assert out[0].candidates_visited + out[1].candidates_visited == one.candidates_visited
+
+
+def test_package_route_errors(gpu):
+    dup = np.array([[1, 0, 0, 1], [1, 0, 0, 1], [0, 0, 1, 1]], dtype=np.uint8)
+    for fn in (gpu.saved_1_gamma, gpu.saved_2_gamma):
+        with pytest.raises(gpu.ValidationError):
+            fn(dup)
+    with pytest.raises(ValueError):
+        gpu.compute_distance(dup, gpu.Algorithm.brute_force)

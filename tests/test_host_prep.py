@@ -199,3 +199,41 @@ def test_library_has_no_oracle_dependency():
     assert "orc_" not in out and "ref_" not in out and "symdist::" not in out
     deps = subprocess.run(["ldd", P.library_path()], capture_output=True, text=True).stdout
     assert "symdist_ref" not in deps and "symdist_oracle" not in deps
+
+
+def test_package_prep_matches_reference_on_random_codes():
+    # diagonalize_f2 (prep.cpp:155-254) and diagonalize_f4 + second_gamma (prep.cpp:256-297):
+    # same matrices, packages and n_pp as the reference library built from its sources
+    import oracle as O
+
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(8)
+    for _ in range(120):
+        n = int(rng.integers(2, 24))
+        k = int(rng.integers(0, n + 1))
+        a = P.generate_code(n, k, int(rng.integers(1, 1 << 40)))
+        for alg in ("saved_1_gamma", "saved_2_gamma"):
+            ref = O.ref_prepare_packages(a, alg)
+            mine = P.prepare_packages(a, P.Algorithm[alg])
+            assert len(ref) == len(mine)
+            for r, m in zip(ref, mine):
+                assert (r["matrix"] == m.matrix).all()
+                assert r["packages"] == m.packages
+                assert r["n_pp"] == m.n_pp
+
+
+def test_package_prep_worked_examples():
+    # test_prep.cpp:24-46: the 3x4 example; test_prep.cpp:84-99 / 131-152: the additive example
+    ex = np.array([[1, 0, 0, 1], [0, 1, 1, 0], [0, 0, 1, 1]], dtype=np.uint8)
+    g = P.diagonalize_f2(ex)
+    assert g.matrix.tolist() == [[1, 0, 0, 1], [0, 1, 0, 1], [0, 0, 1, 1], [1, 0, 1, 0]]
+    assert g.packages == [[0, 2, 3], [1]] and g.pair_count == 2
+    add = np.array([[int(c) for c in r] for r in ("11110000", "00001011", "01110111")], dtype=np.uint8)
+    b, d = P.prepare_packages(add, P.Algorithm.saved_2_gamma)
+    assert b.matrix.tolist() == [[int(c) for c in r] for r in ("11110000", "00001011", "01110111", "11111011")]
+    assert b.packages == [[0, 1, 3], [2]]
+    assert d.matrix.tolist() == [[int(c) for c in r] for r in ("11110000", "10000111", "10001100", "01110111")]
+    assert len(d.packages) == 2 and d.n_pp == 1 and [len(p) for p in d.packages] == [3, 1]
+    with pytest.raises(P.ValidationError):
+        P.diagonalize_f2(np.array([[1, 0, 0, 1], [1, 0, 0, 1], [0, 0, 1, 1]], dtype=np.uint8))
