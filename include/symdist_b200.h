@@ -155,8 +155,9 @@ sdb_status sdb_saved_2_gamma(const uint64_t *rows, int n_rows, int n_cols, int r
                              sdb_trace_entry *trace, int trace_cap, uint64_t *best_out);
 
 /* compute_distance dispatch (distance.cpp:226-240): AUTO runs Saved_2_Gamma when k <= 2 and
- * the isometry route otherwise; SDB_ALG_BRUTE_FORCE returns SDB_ERR_INVALID_ARGUMENT (the
- * brute-force oracle is test infrastructure here, oracle/). */
+ * the isometry route otherwise; SDB_ALG_BRUTE_FORCE is the Gray-code walk over all 2^(n+k)
+ * combinations on the device (brute_force_distance, distance.cpp:151-224; n + k <= 28 like
+ * the reference, SDB_ERR_INVALID_ARGUMENT beyond). */
 sdb_status sdb_compute_distance(const uint64_t *rows, int n_rows, int n_cols, int row_words,
                                 int algorithm, const sdb_run_options *opts, sdb_report *report,
                                 sdb_trace_entry *trace, int trace_cap);

@@ -160,6 +160,33 @@ void package_route_impl(int algorithm, const uint64_t *rows, int n_rows, int n_c
     rep->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// brute_force_distance (distance.cpp:151-224): validate -> Gray walk on the device
+void brute_force_impl(const uint64_t *rows, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
+                      sdb_report *rep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_matrix_args(rows, n_rows, n_cols, row_words);
+    if (n_cols == 0 || n_cols % 2 != 0)
+        throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+    zero_report(rep);
+    const sdb::BitMat a = sdb::BitMat::from_words(rows, n_rows, n_cols, row_words);
+    if (o.validate) {
+        const sdb::Validation v = sdb::validate_normalizer(a);
+        if (!v.ok) throw sdb::ValidationFailure(v.message);
+    }
+    double dev = 0;
+    rep->distance = sdb::run_brute(a, o, &dev);
+    rep->upper = rep->distance;
+    rep->algorithm = SDB_ALG_BRUTE_FORCE;
+    rep->generations = 0;
+    rep->candidates_enumerated = (1ull << n_rows) - 1;
+    rep->candidates_visited = rep->candidates_enumerated;
+    rep->enum_seconds = dev;
+    rep->kernel_launches = 1;
+    rep->complete = 1;
+    rep->workers = 1;
+    rep->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 }  // namespace
 
 struct sdb_plan {
@@ -281,7 +308,8 @@ sdb_status sdb_compute_distance(const uint64_t *rows, int n_rows, int n_cols, in
                 package_route_impl(algorithm, rows, n_rows, n_cols, row_words, o, report, trace, trace_cap, nullptr);
                 return;
             case SDB_ALG_BRUTE_FORCE:
-                throw sdb::InvalidArgument("compute_distance: algorithm not provided by this build yet");
+                brute_force_impl(rows, n_rows, n_cols, row_words, o, report);
+                return;
             default:
                 throw sdb::InvalidArgument("compute_distance: unknown algorithm");
         }

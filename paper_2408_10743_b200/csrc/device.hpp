@@ -174,6 +174,18 @@ struct PkgLevel {
 size_t pkg_smem_bytes(int G, int N, int W, int SW, int P, int BK);
 int launch_pkg_level(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, void *stream, int num_sms);
 
+// Brute force (reference brute_force_distance, distance.cpp:151-224): the Gray-code walk over
+// all 2^rows - 1 combinations of the normalizer rows, one row XOR per step, the C-membership
+// syndrome accumulated alongside; minimum symplectic weight of the admissible ones.
+struct BruteDev {
+    const uint32_t *rows;               // [rows][2W]
+    const unsigned long long *syn;      // [rows] (filter on) bit j = <row_i, row_j>_s
+    unsigned int *best;                 // min weight (atomicMin), ~0u: none
+    int n_rows, W, filter;
+    int block_log2;                     // Gray indices per thread = 2^block_log2
+};
+int launch_brute(const BruteDev &b, void *stream, int num_sms);
+
 // Batch: one code per CTA, the whole level loop on the device.
 struct BatchDev {
     const uint32_t *rows;      // [codes][G][N][2W]

@@ -708,6 +708,65 @@ void Plan::unrank_best(int g, int j, unsigned long long r, std::vector<uint64_t>
 
 // ------------------------------------------------------------------------------- batch
 
+int run_brute(const BitMat &a, const sdb_run_options &o, double *device_seconds) {
+    const int rows = a.rows, n = a.cols / 2, k = rows - n;
+    if (rows > 28) throw InvalidArgument("brute_force_distance: 2^(n+k) enumeration is limited to n+k <= 28 rows");
+    if (rows == 0) throw InvalidArgument("brute_force_distance: matrix has no rows");
+    const int W = (n + 31) / 32;
+    if (W > 4) throw InvalidArgument("brute_force_distance: rows too wide for the brute-force kernel (n > 128)");
+    const bool filter = o.dual_filter && k >= 1;
+    std::vector<uint32_t> h_rows(size_t(rows) * 2 * W, 0);
+    std::vector<unsigned long long> h_syn(size_t(rows), 0);
+    for (int r = 0; r < rows; r++) {
+        extract_bits(a, r, 0, n, h_rows.data() + size_t(r) * 2 * W, W);
+        extract_bits(a, r, n, n, h_rows.data() + size_t(r) * 2 * W + W, W);
+        if (filter)
+            for (int j = 0; j < rows; j++)
+                if (symplectic_ip(a.row(r), a.row(j), n)) h_syn[size_t(r)] |= 1ull << j;
+    }
+    check_cuda(cudaSetDevice(o.device), "cudaSetDevice");
+    int num_sms = 148;
+    check_cuda(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, o.device), "cudaDeviceGetAttribute");
+    cudaStream_t st = o.stream ? static_cast<cudaStream_t>(o.stream) : thread_stream(o.device);
+    const size_t b_rows = align256(h_rows.size() * 4), b_syn = align256(h_syn.size() * 8), bytes = b_rows + b_syn + 256;
+    void *mem = workspace_get(o.device, bytes);
+    unsigned char *base = static_cast<unsigned char *>(mem);
+    BruteDev b{};
+    b.rows = reinterpret_cast<const uint32_t *>(base);
+    b.syn = reinterpret_cast<const unsigned long long *>(base + b_rows);
+    b.best = reinterpret_cast<unsigned int *>(base + b_rows + b_syn);
+    b.n_rows = rows;
+    b.W = W;
+    b.filter = filter ? 1 : 0;
+    b.block_log2 = rows > 20 ? 10 : 4;
+    unsigned best = ~0u;
+    cudaEvent_t e0 = event_get(o.device), e1 = event_get(o.device);
+    try {
+        check_cuda(cudaMemcpyAsync(base, h_rows.data(), h_rows.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+        check_cuda(cudaMemcpyAsync(base + b_rows, h_syn.data(), h_syn.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+        check_cuda(cudaMemsetAsync(b.best, 0xFF, 4, st), "memset");
+        check_cuda(cudaEventRecord(e0, st), "event");
+        if (launch_brute(b, st, num_sms) < 0) throw InvalidArgument("unsupported row width");
+        check_cuda(cudaGetLastError(), "brute kernel launch");
+        check_cuda(cudaEventRecord(e1, st), "event");
+        check_cuda(cudaMemcpyAsync(&best, b.best, 4, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaStreamSynchronize(st), "brute sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (device_seconds) *device_seconds = ms * 1e-3;
+    } catch (...) {
+        event_put(o.device, e0);
+        event_put(o.device, e1);
+        workspace_put(o.device, bytes, mem);
+        throw;
+    }
+    event_put(o.device, e0);
+    event_put(o.device, e1);
+    workspace_put(o.device, bytes, mem);
+    if (best == ~0u) throw InternalFailure("brute_force_distance: no admissible codeword exists");
+    return int(best);
+}
+
 // Batch with the prep on the device (one warp per code). Returns false, having written
 // nothing, when some code needs more Gamma slots than the prep kernel keeps (the caller then
 // runs the host-prep path).

@@ -123,6 +123,10 @@ int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, 
 
 void check_cuda(cudaError_t e, const char *what);
 
+// brute_force_distance (distance.cpp:151-224) on the device; returns the minimum symplectic
+// weight of the admissible combinations (throws InternalFailure when there is none).
+int run_brute(const BitMat &a, const sdb_run_options &o, double *device_seconds);
+
 // Batch of same-shape normalizers, one code per CTA.
 void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
                int *distances, int *statuses, int *generations, sdb_trace_entry *traces, int *trace_lens,

@@ -306,6 +306,45 @@ int launch_pkg_impl(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, cud
     return 1;
 }
 
+// ---------------------------------------------------------------- brute force (Gray walk)
+
+template <int W>
+__global__ void __launch_bounds__(256) brute_kernel(BruteDev b) {
+    __shared__ uint32_t s_rows[32 * 2 * W];
+    __shared__ unsigned long long s_syn[32];
+    for (int i = threadIdx.x; i < b.n_rows * 2 * W; i += blockDim.x) s_rows[i] = b.rows[i];
+    for (int i = threadIdx.x; i < b.n_rows; i += blockDim.x) s_syn[i] = b.filter ? b.syn[i] : 0ull;
+    __syncthreads();
+    const unsigned long long total = (1ull << b.n_rows) - 1;  // m = 1 .. total
+    const unsigned long long nblk = (total + (1ull << b.block_log2)) >> b.block_log2;
+    unsigned best = ~0u;
+    for (unsigned long long blk = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; blk < nblk;
+         blk += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long m0 = max(1ull, blk << b.block_log2);
+        const unsigned long long m1 = min(total + 1, (blk + 1) << b.block_log2);
+        // state after index m0 - 1: the rows of gray(m0 - 1)
+        uint32_t acc[2 * W];
+#pragma unroll
+        for (int w = 0; w < 2 * W; w++) acc[w] = 0;
+        unsigned long long syn = 0;
+        const unsigned long long g0 = (m0 - 1) ^ ((m0 - 1) >> 1);
+        for (int r = 0; r < b.n_rows; r++)
+            if ((g0 >> r) & 1ull) {
+                xor_row<W>(acc, s_rows + r * 2 * W);
+                syn ^= s_syn[r];
+            }
+        for (unsigned long long m = m0; m < m1; m++) {
+            const int flip = __ffsll((long long)m) - 1;
+            xor_row<W>(acc, s_rows + flip * 2 * W);
+            syn ^= s_syn[flip];
+            if (b.filter && syn == 0) continue;
+            best = min(best, unsigned(weight_of<W>(acc)));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_down_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0 && best != ~0u) atomicMin(b.best, best);
+}
+
 // ---------------------------------------------------------------- batch: one code per CTA
 
 template <int W>
@@ -791,6 +830,22 @@ int launch_pkg_level(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, vo
         case 6: return launch_pkg_impl<6>(p, k, L, st, num_sms);
         case 7: return launch_pkg_impl<7>(p, k, L, st, num_sms);
         case 8: return launch_pkg_impl<8>(p, k, L, st, num_sms);
+    }
+    return -1;
+}
+
+int launch_brute(const BruteDev &b, void *stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned long long total = (1ull << b.n_rows) - 1;
+    const unsigned long long nblk = (total + (1ull << b.block_log2)) >> b.block_log2;
+    unsigned long long blocks = (nblk + 255) / 256;
+    if (blocks > (unsigned long long)num_sms * 8) blocks = (unsigned long long)num_sms * 8;
+    if (blocks == 0) blocks = 1;
+    switch (b.W) {
+        case 1: brute_kernel<1><<<unsigned(blocks), 256, 0, st>>>(b); return 1;
+        case 2: brute_kernel<2><<<unsigned(blocks), 256, 0, st>>>(b); return 1;
+        case 3: brute_kernel<3><<<unsigned(blocks), 256, 0, st>>>(b); return 1;
+        case 4: brute_kernel<4><<<unsigned(blocks), 256, 0, st>>>(b); return 1;
     }
     return -1;
 }

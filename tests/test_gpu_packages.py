@@ -108,5 +108,27 @@ def test_package_route_errors(gpu):
     for fn in (gpu.saved_1_gamma, gpu.saved_2_gamma):
         with pytest.raises(gpu.ValidationError):
             fn(dup)
-    with pytest.raises(ValueError):
+    with pytest.raises(gpu.ValidationError):
         gpu.compute_distance(dup, gpu.Algorithm.brute_force)
+
+
+def test_brute_force_on_the_device(gpu):
+    # brute_force_distance (distance.cpp:151-224): the reference's own brute-force answers
+    gd = load_golden("reference_kats.json")
+    for case in gd["cases"]:
+        a = hex_to_mat(case["normalizer"], 2 * case["n"])
+        rep = gpu.compute_distance(a, gpu.Algorithm.brute_force)
+        assert rep.distance == case["brute"]
+        assert rep.algorithm == gpu.Algorithm.brute_force
+        assert rep.candidates_enumerated == (1 << a.shape[0]) - 1 and rep.generations == 0
+    # config 1 (28 rows, the reference's limit) and the limit itself
+    c1 = load_golden("config1.json")
+    a = hex_to_mat(c1["normalizer"], 2 * c1["n"])
+    assert gpu.compute_distance(a, gpu.Algorithm.brute_force).distance == c1["distance"]
+    with pytest.raises(ValueError):
+        gpu.compute_distance(gpu.generate_code(25, 4, 1), gpu.Algorithm.brute_force)
+    # filter off: plain minimum weight over the whole row space
+    a = gpu.generate_code(10, 3, 77)
+    plain = gpu.compute_distance(a, gpu.Algorithm.brute_force, gpu.RunOptions(dual_filter=False))
+    import oracle as O
+    assert plain.distance == O.brute_force(a, dual_filter=False)
