@@ -31,6 +31,9 @@
  *   sdb_saved_isometry_batch  (no reference counterpart: a loop of saved_isometry
  *                              calls, one code per CTA on the GPU; BASELINE config 3)
  *   sdb_generate_code       (BASELINE.md §2 seeded config generator)
+ *   sdb_random_stabilizer   symdist::random_stabilizer   include/symdist/distance.hpp:80
+ *   sdb_parse_matrix_text   symdist::parse_matrix_text   include/symdist/matrix_io.hpp:13-14
+ *   sdb_format_matrix       symdist::format_matrix       include/symdist/matrix_io.hpp:18
  *   sdb_plan_*              device-resident split of sdb_saved_isometry: prep + H2D once,
  *                           then the level loop from HBM (used to time the kernel path alone)
  *
@@ -226,6 +229,19 @@ sdb_status sdb_prepare_packages(const uint64_t *rows, int n_rows, int n_cols, in
  * <= 0 means 4n. */
 sdb_status sdb_generate_code(int n, int k, uint64_t seed, int transvections, uint64_t *out,
                              int out_row_words);
+
+/* random_stabilizer (distance.cpp:242-294): the reference's mt19937_64 instance generator,
+ * same draws; (n+k) x 2n into out. */
+sdb_status sdb_random_stabilizer(int n, int k, uint64_t seed, uint64_t *out, int out_row_words);
+
+/* Matrix text format (matrix_io.cpp:26-106, matrix_io.hpp:13-18): "K N" header then K rows of
+ * N '0'/'1' characters. Parse failures return SDB_ERR_PARSE with the reference's
+ * "origin:line: what" message. out may be NULL to query the shape. format_matrix writes the
+ * inverse text (NUL-terminated) when buf is non-NULL; *len = its length. */
+sdb_status sdb_parse_matrix_text(const char *text, const char *origin, uint64_t *out, int out_row_words,
+                                 int max_rows, int *n_rows, int *n_cols);
+sdb_status sdb_format_matrix(const uint64_t *rows, int n_rows, int n_cols, int row_words, char *buf, int cap,
+                             int *len);
 
 /* ---- device-resident plan (prep + H2D once, levels from HBM) ---------------------- */
 typedef struct sdb_plan sdb_plan;

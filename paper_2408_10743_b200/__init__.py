@@ -22,6 +22,9 @@ this module                            reference
 ``lower_bound``                        ``lower_bound`` engine.cpp:31-47
 ``run_bz``                             ``run_bz`` engine.cpp:303-343 (singleton packages)
 ``saved_isometry_batch``               (loop of saved_isometry; one code per CTA)
+``random_stabilizer``                  ``random_stabilizer`` distance.cpp:242-294
+``parse_matrix_text`` / ``format_matrix``  matrix_io.cpp:26-106
+``cli_path()`` (``symdist_b200``)      the CLI, tools/symdist_main.cpp
 =====================================  ==================================================
 
 Errors: ``ValidationError``, ``InternalError``, ``ParseError`` mirror symdist/errors.hpp;
@@ -43,7 +46,8 @@ __all__ = [
     "Algorithm", "WeightMode", "StabilizerInstance", "RunOptions", "DistanceReport", "BoundsTraceEntry",
     "BoundsState", "PackagedGamma", "AdmissibilityFilter", "ValidationResult", "ParseError", "ValidationError",
     "InternalError", "DeviceError", "saved_isometry", "saved_1_gamma", "saved_2_gamma", "compute_distance",
-    "diagonalize_f2", "prepare_packages", "saved_isometry_batch", "run_bz",
+    "diagonalize_f2", "prepare_packages", "random_stabilizer", "parse_matrix_text", "parse_matrix_file",
+    "format_matrix", "cli_path", "saved_isometry_batch", "run_bz",
     "lower_bound", "validate_normalizer", "isometry_transform", "information_sets", "singleton_gamma",
     "generate_code", "Plan", "pack_rows", "unpack_rows", "library", "library_path", "device_available", "CONFIGS",
 ]
@@ -128,6 +132,7 @@ _EXPORTS = [
     "sdb_compute_distance", "sdb_saved_isometry_batch", "sdb_run_bz", "sdb_lower_bound", "sdb_validate_normalizer",
     "sdb_isometry_transform", "sdb_information_sets", "sdb_generate_code", "sdb_plan_create", "sdb_plan_run",
     "sdb_plan_destroy", "sdb_saved_1_gamma", "sdb_saved_2_gamma", "sdb_run_bz_packaged", "sdb_prepare_packages",
+    "sdb_random_stabilizer", "sdb_parse_matrix_text", "sdb_format_matrix",
 ]
 
 
@@ -150,6 +155,9 @@ def library():
                                      C.POINTER(C.c_double)]
         lib.sdb_plan_destroy.argtypes = [C.c_void_p]
         lib.sdb_generate_code.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p, C.c_int]
+        lib.sdb_random_stabilizer.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_int]
+        lib.sdb_parse_matrix_text.argtypes = [C.c_char_p, C.c_char_p, C.c_void_p, C.c_int, C.c_int,
+                                              C.POINTER(C.c_int), C.POINTER(C.c_int)]
         _lib = lib
     return _lib
 
@@ -662,6 +670,52 @@ def _run_bz_packaged(gammas, filt, opts):
                        candidates_enumerated=r.candidates_enumerated, trace=r.trace_tuples(),
                        best=unpack_rows(best.reshape(1, -1), cols)[0] if r.best_generation > 0 else np.zeros(0, np.uint8),
                        report=r)
+
+
+def random_stabilizer(n: int, k: int, seed: int) -> StabilizerInstance:
+    """The reference's instance generator (distance.cpp:242-294), same mt19937_64 draws."""
+    words = max(1, (2 * n + 63) // 64)
+    out = np.zeros((max(n + k, 1), words), dtype=np.uint64)
+    _raise(library().sdb_random_stabilizer(n, k, C.c_uint64(seed), out.ctypes.data, words))
+    return StabilizerInstance.from_matrix(unpack_rows(out[:n + k], 2 * n))
+
+
+def parse_matrix_text(text: str, origin: str = "<input>") -> StabilizerInstance:
+    """matrix_io.cpp:26-89: "K N" header then K rows of N '0'/'1' (ParseError on bad input)."""
+    t = text.encode()
+    o = origin.encode()
+    nr, nc = C.c_int(0), C.c_int(0)
+    lib = library()
+    _raise(lib.sdb_parse_matrix_text(t, o, None, 0, 0, C.byref(nr), C.byref(nc)))
+    words = max(1, (nc.value + 63) // 64)
+    out = np.zeros((max(nr.value, 1), words), dtype=np.uint64)
+    _raise(lib.sdb_parse_matrix_text(t, o, out.ctypes.data, words, nr.value, C.byref(nr), C.byref(nc)))
+    return StabilizerInstance.from_matrix(unpack_rows(out[:nr.value], nc.value))
+
+
+def parse_matrix_file(path: str) -> StabilizerInstance:
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        raise ParseError(f"{path}: cannot open file") from None
+    return parse_matrix_text(text, path)
+
+
+def format_matrix(m) -> str:
+    a = np.asarray(m.a if isinstance(m, StabilizerInstance) else m, dtype=np.uint8)
+    w = pack_rows(a)
+    ln = C.c_int(0)
+    lib = library()
+    _raise(lib.sdb_format_matrix(_wptr(w), a.shape[0], a.shape[1], w.shape[1], None, 0, C.byref(ln)))
+    buf = C.create_string_buffer(ln.value + 1)
+    _raise(lib.sdb_format_matrix(_wptr(w), a.shape[0], a.shape[1], w.shape[1], buf, ln.value + 1, C.byref(ln)))
+    return buf.value.decode()
+
+
+def cli_path() -> str:
+    """The symdist_b200 CLI (compute / verify / bench, reference tools/symdist_main.cpp)."""
+    return os.path.join(HERE, "symdist_b200")
 
 
 def generate_code(n: int, k: int, seed: int, transvections: int = 0) -> np.ndarray:

@@ -479,6 +479,42 @@ sdb_status sdb_information_sets(const uint64_t *rows, int n_rows, int n_cols, in
     });
 }
 
+sdb_status sdb_random_stabilizer(int n, int k, uint64_t seed, uint64_t *out, int out_row_words) {
+    return guarded([&] {
+        if (!out) throw sdb::InvalidArgument("null output");
+        const sdb::BitMat a = sdb::random_stabilizer(n, k, seed);
+        if (out_row_words < a.stride) throw sdb::InvalidArgument("out_row_words too small");
+        a.to_words(out, out_row_words);
+    });
+}
+
+sdb_status sdb_parse_matrix_text(const char *text, const char *origin, uint64_t *out, int out_row_words, int max_rows,
+                                 int *n_rows, int *n_cols) {
+    return guarded([&] {
+        if (!text || !n_rows || !n_cols) throw sdb::InvalidArgument("null argument");
+        const sdb::BitMat m = sdb::parse_matrix_text(text, origin ? origin : "<input>");
+        *n_rows = m.rows;
+        *n_cols = m.cols;
+        if (out) {
+            if (m.rows > max_rows || out_row_words < m.stride) throw sdb::InvalidArgument("output buffer too small");
+            m.to_words(out, out_row_words);
+        }
+    });
+}
+
+sdb_status sdb_format_matrix(const uint64_t *rows, int n_rows, int n_cols, int row_words, char *buf, int cap,
+                             int *len) {
+    return guarded([&] {
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        const std::string s = sdb::format_matrix(sdb::BitMat::from_words(rows, n_rows, n_cols, row_words));
+        if (len) *len = int(s.size());
+        if (buf) {
+            if (cap < int(s.size()) + 1) throw sdb::InvalidArgument("buffer too small");
+            std::memcpy(buf, s.c_str(), s.size() + 1);
+        }
+    });
+}
+
 sdb_status sdb_generate_code(int n, int k, uint64_t seed, int transvections, uint64_t *out, int out_row_words) {
     return guarded([&] {
         if (!out) throw sdb::InvalidArgument("null output");

@@ -1,6 +1,9 @@
 #include "gf2.hpp"
 
 #include <algorithm>
+#include <cctype>
+#include <random>
+#include <sstream>
 #include <stdexcept>
 
 #include "errors.hpp"
@@ -200,6 +203,116 @@ BitMat generate_code(int n, int k, uint64_t seed, int transvections) {
             }
     }
     return a;
+}
+
+BitMat random_stabilizer(int n, int k, uint64_t seed) {
+    if (n <= 0 || k < 0 || k > n) throw InvalidArgument("random_stabilizer: need 0 <= k <= n, n >= 1");
+    std::mt19937_64 rng(seed);
+    const int cols = 2 * n, dim_c = n - k;
+    BitMat c(0, cols), ech(0, cols);
+    std::vector<int> pivots;
+    auto append = [](BitMat &m, const uint64_t *row) {
+        m.w.insert(m.w.end(), row, row + m.stride);
+        m.rows++;
+    };
+    while (c.rows < dim_c) {
+        // uniform draw from the symplectic complement of the rows so far
+        const BitMat basis = null_space(swap_halves(c));
+        for (;;) {
+            std::vector<uint64_t> v(size_t(c.stride), 0);
+            const int dim = basis.rows;
+            std::vector<uint64_t> draw(size_t((dim + 63) / 64));
+            for (uint64_t &x : draw) x = rng();
+            for (int i = 0; i < dim; i++)
+                if ((draw[size_t(i / 64)] >> (i % 64)) & 1u)
+                    for (int w = 0; w < c.stride; w++) v[size_t(w)] ^= basis.row(i)[w];
+            std::vector<uint64_t> res(v);
+            for (int r = 0; r < ech.rows; r++)
+                if ((res[size_t(pivots[size_t(r)] >> 6)] >> (pivots[size_t(r)] & 63)) & 1u)
+                    for (int w = 0; w < c.stride; w++) res[size_t(w)] ^= ech.row(r)[w];
+            int pivot = -1;
+            for (int b = 0; b < cols && pivot < 0; b++)
+                if ((res[size_t(b >> 6)] >> (b & 63)) & 1u) pivot = b;
+            if (pivot < 0) continue;  // dependent draw
+            append(c, v.data());
+            append(ech, res.data());
+            pivots.push_back(pivot);
+            break;
+        }
+    }
+    return null_space(swap_halves(c));
+}
+
+namespace {
+[[noreturn]] void parse_fail(const std::string &origin, size_t line, const std::string &what) {
+    throw ParseFailure(origin + ":" + std::to_string(line) + ": " + what);
+}
+bool blank_line(const std::string &s) {
+    for (char ch : s)
+        if (!std::isspace(static_cast<unsigned char>(ch))) return false;
+    return true;
+}
+}  // namespace
+
+BitMat parse_matrix_text(const std::string &text, const std::string &origin) {
+    std::istringstream in(text);
+    std::string line;
+    size_t line_no = 0;
+    long k_rows = -1, n_cols = -1;
+    while (std::getline(in, line)) {
+        ++line_no;
+        if (blank_line(line)) continue;
+        std::istringstream header(line);
+        std::string extra;
+        if (!(header >> k_rows >> n_cols) || (header >> extra))
+            parse_fail(origin, line_no, "bad header; expected two integers \"K N\"");
+        break;
+    }
+    if (k_rows < 0) parse_fail(origin, line_no, "empty input; expected a \"K N\" header");
+    if (k_rows == 0 || n_cols <= 0) parse_fail(origin, line_no, "bad header; K and N must be positive");
+    if (n_cols % 2 != 0) parse_fail(origin, line_no, "N must be even (columns come in symplectic pairs)");
+    if (k_rows > n_cols) parse_fail(origin, line_no, "K exceeds N; rows cannot be independent");
+    BitMat m(0, int(n_cols));
+    std::vector<uint64_t> row(size_t(m.stride));
+    long rows_read = 0;
+    while (std::getline(in, line)) {
+        ++line_no;
+        if (blank_line(line)) continue;
+        if (rows_read == k_rows) parse_fail(origin, line_no, "expected " + std::to_string(k_rows) + " rows, found more");
+        std::fill(row.begin(), row.end(), 0);
+        long bits = 0;
+        for (size_t col = 0; col < line.size(); ++col) {
+            const char ch = line[col];
+            if (std::isspace(static_cast<unsigned char>(ch))) continue;
+            if (ch != '0' && ch != '1')
+                parse_fail(origin, line_no,
+                           "row " + std::to_string(rows_read + 1) + ", column " + std::to_string(col + 1) +
+                               ": expected '0' or '1', found '" + std::string(1, ch) + "'");
+            if (bits == n_cols)
+                parse_fail(origin, line_no,
+                           "row " + std::to_string(rows_read + 1) + " has more than " + std::to_string(n_cols) +
+                               " bits");
+            if (ch == '1') row[size_t(bits >> 6)] |= uint64_t(1) << (bits & 63);
+            ++bits;
+        }
+        if (bits != n_cols)
+            parse_fail(origin, line_no,
+                       "row " + std::to_string(rows_read + 1) + " has " + std::to_string(bits) + " bits, expected " +
+                           std::to_string(n_cols));
+        m.w.insert(m.w.end(), row.begin(), row.end());
+        m.rows++;
+        ++rows_read;
+    }
+    if (rows_read != k_rows)
+        parse_fail(origin, line_no,
+                   "expected " + std::to_string(k_rows) + " rows, found " + std::to_string(rows_read));
+    return m;
+}
+
+std::string format_matrix(const BitMat &m) {
+    std::string out = std::to_string(m.rows) + " " + std::to_string(m.cols) + "\n";
+    for (int r = 0; r < m.rows; r++) out += m.row_string(r) + "\n";
+    return out;
 }
 
 }  // namespace sdb

@@ -75,6 +75,16 @@ std::vector<InfoSet> information_sets(const BitMat &b);
 // BASELINE.md §2 generator (xorshift64* transvections on the canonical generators).
 BitMat generate_code(int n, int k, uint64_t seed, int transvections);
 
+// random_stabilizer (distance.cpp:242-294): mt19937_64(seed) grows a self-orthogonal C, the
+// normalizer is a basis of its symplectic dual. Same draws, same null-space order.
+BitMat random_stabilizer(int n, int k, uint64_t seed);
+
+// Matrix text format (matrix_io.cpp:26-106): "K N" header, K rows of N characters '0'/'1';
+// whitespace inside rows and blank lines ignored. Throws ParseFailure with the reference's
+// "origin:line: what" diagnostics.
+BitMat parse_matrix_text(const std::string &text, const std::string &origin);
+std::string format_matrix(const BitMat &m);
+
 // <u,v>_s over the first 2n columns of both (n = pair count).
 int symplectic_ip(const uint64_t *u, const uint64_t *v, int n);
 
