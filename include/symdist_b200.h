@@ -34,6 +34,8 @@
  *   sdb_random_stabilizer   symdist::random_stabilizer   include/symdist/distance.hpp:80
  *   sdb_parse_matrix_text   symdist::parse_matrix_text   include/symdist/matrix_io.hpp:13-14
  *   sdb_format_matrix       symdist::format_matrix       include/symdist/matrix_io.hpp:18
+ *   sdb_comm_*              NCCL communicator for the per-level min-allreduce (multi-GPU;
+ *                           the reference's in-process CAS-min, engine.cpp:178-181, across GPUs)
  *   sdb_plan_*              device-resident split of sdb_saved_isometry: prep + H2D once,
  *                           then the level loop from HBM (used to time the kernel path alone)
  *
@@ -55,7 +57,7 @@
 extern "C" {
 #endif
 
-#define SDB_ABI_VERSION 1
+#define SDB_ABI_VERSION 2
 
 typedef enum {
     SDB_OK = 0,
@@ -105,7 +107,11 @@ typedef struct {
     int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel, 2 force the tile kernel,
                                3 batch only: run the prep (validation, information sets) on the host */
     void *stream;           /* cudaStream_t to run on (NULL: a private non-blocking stream) */
-    int reserved[6];
+    void *comm;             /* sdb_comm_create handle (NCCL): with world > 1 the level exchange is a
+                               stream-ordered min-allreduce, no host round trip (else allreduce_min) */
+    long long shard_min;    /* levels with fewer candidates run whole on every rank, no exchange
+                               (0: default 2^30; 1: shard every level) */
+    int reserved[4];
 } sdb_run_options;
 
 /* symdist::DistanceReport (distance.hpp:44-52) plus GPU-side measurements. */
@@ -242,6 +248,16 @@ sdb_status sdb_parse_matrix_text(const char *text, const char *origin, uint64_t 
                                  int max_rows, int *n_rows, int *n_cols);
 sdb_status sdb_format_matrix(const uint64_t *rows, int n_rows, int n_cols, int row_words, char *buf, int cap,
                              int *len);
+
+/* ---- multi-GPU: NCCL communicator for the per-level exchange ------------------------ */
+/* Rank 0 makes the id and shares it out of band (bench.py: torch.distributed broadcast);
+ * every rank then creates its communicator on its device. */
+sdb_status sdb_comm_unique_id(unsigned char id[128]);
+sdb_status sdb_comm_create(const unsigned char id[128], int rank, int world, int device, void **comm);
+void sdb_comm_destroy(void *comm);
+/* Synchronous elementwise min of count host uint64 values across the communicator (the
+ * plumbing of the per-level exchange; usable as an sdb_allreduce_min_fn body). */
+sdb_status sdb_comm_allreduce_min(void *comm, uint64_t *values, int count, int device);
 
 /* ---- device-resident plan (prep + H2D once, levels from HBM) ---------------------- */
 typedef struct sdb_plan sdb_plan;

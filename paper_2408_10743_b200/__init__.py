@@ -47,7 +47,7 @@ __all__ = [
     "BoundsState", "PackagedGamma", "AdmissibilityFilter", "ValidationResult", "ParseError", "ValidationError",
     "InternalError", "DeviceError", "saved_isometry", "saved_1_gamma", "saved_2_gamma", "compute_distance",
     "diagonalize_f2", "prepare_packages", "random_stabilizer", "parse_matrix_text", "parse_matrix_file",
-    "format_matrix", "cli_path", "saved_isometry_batch", "run_bz",
+    "format_matrix", "cli_path", "Comm", "saved_isometry_batch", "run_bz",
     "lower_bound", "validate_normalizer", "isometry_transform", "information_sets", "singleton_gamma",
     "generate_code", "Plan", "pack_rows", "unpack_rows", "library", "library_path", "device_available", "CONFIGS",
 ]
@@ -109,7 +109,8 @@ class _Options(C.Structure):
     _fields_ = [
         ("workers", C.c_int), ("validate", C.c_int), ("dual_filter", C.c_int), ("device", C.c_int),
         ("max_generation", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("allreduce_min", _ALLREDUCE),
-        ("allreduce_ctx", C.c_void_p), ("kernel", C.c_int), ("stream", C.c_void_p), ("reserved", C.c_int * 6),
+        ("allreduce_ctx", C.c_void_p), ("kernel", C.c_int), ("stream", C.c_void_p), ("comm", C.c_void_p),
+        ("shard_min", C.c_longlong), ("reserved", C.c_int * 4),
     ]
 
 
@@ -132,7 +133,8 @@ _EXPORTS = [
     "sdb_compute_distance", "sdb_saved_isometry_batch", "sdb_run_bz", "sdb_lower_bound", "sdb_validate_normalizer",
     "sdb_isometry_transform", "sdb_information_sets", "sdb_generate_code", "sdb_plan_create", "sdb_plan_run",
     "sdb_plan_destroy", "sdb_saved_1_gamma", "sdb_saved_2_gamma", "sdb_run_bz_packaged", "sdb_prepare_packages",
-    "sdb_random_stabilizer", "sdb_parse_matrix_text", "sdb_format_matrix",
+    "sdb_random_stabilizer", "sdb_parse_matrix_text", "sdb_format_matrix", "sdb_comm_unique_id", "sdb_comm_create",
+    "sdb_comm_destroy", "sdb_comm_allreduce_min",
 ]
 
 
@@ -154,6 +156,9 @@ def library():
         lib.sdb_plan_run.argtypes = [C.c_void_p, C.POINTER(_Report), C.POINTER(_Trace), C.c_int,
                                      C.POINTER(C.c_double)]
         lib.sdb_plan_destroy.argtypes = [C.c_void_p]
+        lib.sdb_comm_destroy.argtypes = [C.c_void_p]
+        lib.sdb_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        lib.sdb_comm_allreduce_min.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         lib.sdb_generate_code.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p, C.c_int]
         lib.sdb_random_stabilizer.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_int]
         lib.sdb_parse_matrix_text.argtypes = [C.c_char_p, C.c_char_p, C.c_void_p, C.c_int, C.c_int,
@@ -242,6 +247,8 @@ class RunOptions:
     allreduce_min: Optional[Callable[[np.ndarray], np.ndarray]] = None
     kernel: int = 0  # 0 auto, 1 walk, 2 tile
     stream: int = 0  # cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream); 0 = private
+    comm: int = 0  # Comm.handle (NCCL): the level exchange runs on the stream, no host round trip
+    shard_min: int = 0  # levels below this many candidates run whole on every rank (0: 2^30)
 
     def _c(self) -> tuple[_Options, object]:
         o = _Options()
@@ -254,6 +261,8 @@ class RunOptions:
         o.world = self.world
         o.kernel = self.kernel
         o.stream = self.stream or None
+        o.comm = self.comm or None
+        o.shard_min = self.shard_min
         keep = None
         if self.allreduce_min is not None:
             fn = self.allreduce_min
@@ -711,6 +720,34 @@ def format_matrix(m) -> str:
     buf = C.create_string_buffer(ln.value + 1)
     _raise(lib.sdb_format_matrix(_wptr(w), a.shape[0], a.shape[1], w.shape[1], buf, ln.value + 1, C.byref(ln)))
     return buf.value.decode()
+
+
+class Comm:
+    """NCCL communicator for the per-level exchange across GPUs (one per process/GPU).
+    ``Comm.unique_id()`` on rank 0, shared out of band, then ``Comm(uid, rank, world, device)``
+    on every rank; pass ``comm.handle`` as ``RunOptions.comm``."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _raise(library().sdb_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid: bytes, rank: int, world: int, device: int = 0):
+        h = C.c_void_p()
+        _raise(library().sdb_comm_create(uid, rank, world, device, C.byref(h)))
+        self.handle = h.value
+        self.device = device
+
+    def allreduce_min(self, values) -> np.ndarray:
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.uint64)).copy()
+        _raise(library().sdb_comm_allreduce_min(self.handle, v.ctypes.data, len(v), self.device))
+        return v
+
+    def close(self):
+        if getattr(self, "handle", None):
+            library().sdb_comm_destroy(self.handle)
+            self.handle = None
 
 
 def cli_path() -> str:

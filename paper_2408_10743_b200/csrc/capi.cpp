@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/symdist_b200.h"
+#include "comm.hpp"
 #include "engine.hpp"
 #include "errors.hpp"
 #include "gf2.hpp"
@@ -573,6 +574,45 @@ sdb_status sdb_plan_run(sdb_plan *plan, sdb_report *report, sdb_trace_entry *tra
         report->prep_seconds = plan->prep_seconds;
         report->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
+}
+
+sdb_status sdb_comm_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        if (!id) throw sdb::InvalidArgument("null id");
+        sdb::comm_unique_id(id);
+    });
+}
+
+sdb_status sdb_comm_create(const unsigned char id[128], int rank, int world, int device, void **comm) {
+    return guarded([&] {
+        if (!id || !comm) throw sdb::InvalidArgument("null argument");
+        *comm = sdb::comm_create(id, rank, world, device);
+    });
+}
+
+sdb_status sdb_comm_allreduce_min(void *comm, uint64_t *values, int count, int device) {
+    return guarded([&] {
+        if (!comm || (!values && count > 0) || count < 0) throw sdb::InvalidArgument("null argument");
+        sdb::check_cuda(cudaSetDevice(device), "cudaSetDevice");
+        unsigned long long *d = nullptr;
+        sdb::check_cuda(cudaMalloc(&d, size_t(std::max(count, 1)) * 8), "cudaMalloc");
+        try {
+            sdb::check_cuda(cudaMemcpy(d, values, size_t(count) * 8, cudaMemcpyHostToDevice), "H2D");
+            sdb::comm_allreduce_min_u64(comm, d, size_t(count), nullptr);
+            sdb::check_cuda(cudaMemcpy(values, d, size_t(count) * 8, cudaMemcpyDeviceToHost), "D2H");
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        cudaFree(d);
+    });
+}
+
+void sdb_comm_destroy(void *comm) {
+    try {
+        sdb::comm_destroy(comm);
+    } catch (...) {
+    }
 }
 
 void sdb_plan_destroy(sdb_plan *plan) {

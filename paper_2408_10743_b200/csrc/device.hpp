@@ -80,7 +80,7 @@ struct LevelLaunch {
 // close one level (fold the level minimum into U, trace, termination, reset the level).
 int launch_run_init(const ProblemDev &p, unsigned sentinel, const unsigned long long *counter_init,
                     unsigned long long *counters, int n_counters, void *stream);
-int launch_level_close(const ProblemDev &p, int g, long long lower, void *stream);
+int launch_level_close(const ProblemDev &p, int g, long long lower, int from_keys, void *stream);
 
 // One level, all matrices, lexicographic-walk kernel. Returns the number of kernels launched.
 int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, int num_sms);

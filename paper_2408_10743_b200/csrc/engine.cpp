@@ -8,6 +8,7 @@
 #include <mutex>
 #include <thread>
 
+#include "comm.hpp"
 #include "errors.hpp"
 
 namespace sdb {
@@ -457,7 +458,12 @@ unsigned long long Plan::level_candidates(int g) const {
 void Plan::prepare_level(int g) {
     LevelHost &lv = levels_[size_t(g)];
     if (lv.ready) return;
-    const int world = std::max(1, opts_.world), rank = opts_.rank;
+    // small levels run whole on every rank (identical results, no exchange); big ones shard
+    const unsigned long long shard_min = opts_.shard_min > 0 ? (unsigned long long)opts_.shard_min : (1ull << 30);
+    // (a one-rank communicator with shard_min = 1 takes the exchange path too: the single-GPU
+    // test of the NCCL plumbing)
+    lv.sharded = (opts_.world > 1 || (opts_.comm && opts_.shard_min == 1)) && level_candidates(g) >= shard_min;
+    const int world = lv.sharded ? std::max(1, opts_.world) : 1, rank = lv.sharded ? opts_.rank : 0;
     if (packaged_) {
         if (g >= BK_) throw InvalidArgument("generation beyond the kernels' combination-size limit");
         PkgLevel &L = lv.pkg;
@@ -550,7 +556,8 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     check_cuda(cudaSetDevice(device_), "cudaSetDevice");
     const int world = std::max(1, opts_.world), rank = opts_.rank;
     if (rank < 0 || rank >= world) throw InvalidArgument("rank outside [0, world)");
-    if (world > 1 && !opts_.allreduce_min) throw InvalidArgument("world > 1 needs an allreduce_min callback");
+    if (world > 1 && !opts_.allreduce_min && !opts_.comm)
+        throw InvalidArgument("world > 1 needs a communicator (comm) or an allreduce_min callback");
     // every matrix generates the full code: the smallest package count closes the search
     // (engine.cpp:322-325)
     int g_limit = N_;
@@ -574,9 +581,15 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         if (nl < 0) throw InvalidArgument("unsupported row width");
         launches += nl;
         check_cuda(cudaGetLastError(), "level kernel launch");
-        if (world > 1) {
-            // min-allreduce of (level minimum, its key) across ranks, then hand the result
-            // to level_close through the same state fields
+        int from_keys = 0;
+        if (lv.sharded && opts_.comm) {
+            // stream-ordered NCCL min-allreduce of the per-weight best keys; level_close reads
+            // the level minimum off them
+            comm_allreduce_min_u64(opts_.comm, pd_.key_by_w, size_t(max_weight_ + 1), stream_);
+            from_keys = 1;
+        } else if (lv.sharded) {
+            // min-allreduce of (level minimum, its key) across ranks through the host
+            // callback, then hand the result to level_close through the same state fields
             const size_t sb = sizeof(LevelState) + size_t(max_weight_ + 1) * 8;
             h_state.resize(sb);
             check_cuda(cudaMemcpyAsync(h_state.data(), pd_.state, sb, cudaMemcpyDeviceToHost, stream_), "D2H state");
@@ -602,12 +615,12 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
                 h2d += 8;
             }
         }
-        launches += launch_level_close(pd_, g, lower_bound(g), stream_);
+        launches += launch_level_close(pd_, g, lower_bound(g), from_keys, stream_);
         check_cuda(cudaGetLastError(), "level close launch");
         check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
         last_g = g;
         const unsigned long long total = level_candidates(g);
-        if (world > 1 || total >= kSyncCandidates || g == g_limit) {
+        if ((lv.sharded && !opts_.comm) || total >= kSyncCandidates || g == g_limit) {
             check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
             check_cuda(cudaStreamSynchronize(stream_), "level sync");
             d2h += sizeof ctl;

@@ -61,6 +61,7 @@ class Plan {
     // host-side launch description of one level, built the first time a run reaches it
     struct LevelHost {
         bool ready = false;
+        bool sharded = false;         // split across ranks (else every rank runs it whole)
         int t = 0;                    // 0: walk kernel, else the tile kernel's tail size
         LevelLaunch walk{};
         TilePlan tile{};

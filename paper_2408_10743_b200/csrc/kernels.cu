@@ -90,11 +90,21 @@ __global__ void run_init_kernel(ProblemDev p, unsigned sentinel, const unsigned 
 
 // Reference run_bz level barrier (engine.cpp:327-335): U from the level minimum (admissible
 // candidates only, already filtered in the kernels), trace entry, stop when L >= U.
-__global__ void level_close_kernel(ProblemDev p, int g, long long lower) {
+__global__ void level_close_kernel(ProblemDev p, int g, long long lower, int from_keys) {
+    __shared__ unsigned s_w;
+    if (from_keys) {
+        // after the cross-rank min-allreduce of key_by_w: the level minimum is the smallest
+        // weight any rank keyed
+        if (threadIdx.x == 0) s_w = ~0u;
+        __syncthreads();
+        for (int i = threadIdx.x; i <= p.max_weight; i += blockDim.x)
+            if (p.key_by_w[i] != ~0ull) atomicMin(&s_w, unsigned(i));
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
         RunCtl *c = p.ctl;
         if (!c->done) {
-            const unsigned w = p.state->wmin;
+            const unsigned w = from_keys ? s_w : p.state->wmin;
             if (w != ~0u && w < c->U) {
                 c->U = w;
                 c->best_g = g;
@@ -778,8 +788,8 @@ int launch_run_init(const ProblemDev &p, unsigned sentinel, const unsigned long 
     return 1;
 }
 
-int launch_level_close(const ProblemDev &p, int g, long long lower, void *stream) {
-    level_close_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, g, lower);
+int launch_level_close(const ProblemDev &p, int g, long long lower, int from_keys, void *stream) {
+    level_close_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, g, lower, from_keys);
     return 1;
 }
 size_t tile_smem_bytes(int G, int N, int W, int SW, int BK) { return tile_smem(G, N, W, SW, BK); }

@@ -91,7 +91,7 @@ def test_run_bz_with_prepared_packages(gpu):
     out = [None, None]
 
     def run(r):
-        out[r] = gpu.saved_2_gamma(a, gpu.RunOptions(rank=r, world=2, allreduce_min=fn_for(r)))
+        out[r] = gpu.saved_2_gamma(a, gpu.RunOptions(rank=r, world=2, allreduce_min=fn_for(r), shard_min=1))
 
     ths = [threading.Thread(target=run, args=(r,)) for r in range(2)]
     for t in ths:

@@ -53,7 +53,7 @@ def test_sharded_levels_match_single(gpu, world):
     out = [None] * world
 
     def run(r):
-        out[r] = gpu.saved_isometry(a, gpu.RunOptions(rank=r, world=world, allreduce_min=ar.fn_for(r)),
+        out[r] = gpu.saved_isometry(a, gpu.RunOptions(rank=r, world=world, allreduce_min=ar.fn_for(r), shard_min=1),
                                     return_best=True)
 
     ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
@@ -77,3 +77,39 @@ def test_plan_reuse_is_deterministic(gpu):
     assert tr(r1) == tr(r2)
     assert r1.distance == 7
     assert len(r1.level_seconds) == len(r1.bounds_trace)
+
+
+def test_small_levels_run_whole_on_every_rank(gpu):
+    # below shard_min a level runs whole on every rank with no exchange: same answer, and each
+    # rank visits every candidate of those levels
+    c = gpu.CONFIGS[2]
+    a = gpu.generate_code(c["n"], c["k"], c["seed"])
+    single = gpu.saved_isometry(a)
+    calls = []
+
+    def never(v):
+        calls.append(1)
+        return v
+
+    rep = gpu.saved_isometry(a, gpu.RunOptions(rank=1, world=2, allreduce_min=never))
+    assert tr(rep) == tr(single) and not calls
+    assert rep.candidates_visited == single.candidates_visited
+
+
+def test_nccl_exchange_path_on_one_gpu(gpu):
+    # a one-rank NCCL communicator with shard_min = 1 runs every level through the
+    # stream-ordered min-allreduce of the per-weight keys and level_close's key scan
+    comm = gpu.Comm(gpu.Comm.unique_id(), 0, 1, 0)
+    try:
+        v = comm.allreduce_min([5, 3, 2**64 - 1])
+        assert v.tolist() == [5, 3, 2**64 - 1]
+        for cid in (1, 2, 4):
+            c = gpu.CONFIGS[cid]
+            a = gpu.generate_code(c["n"], c["k"], c["seed"])
+            base, best0 = gpu.saved_isometry(a, return_best=True)
+            via, best1 = gpu.saved_isometry(a, gpu.RunOptions(comm=comm.handle, shard_min=1), return_best=True)
+            assert tr(via) == tr(base) and (best0 == best1).all()
+        g2 = gpu.saved_2_gamma(a, gpu.RunOptions(comm=comm.handle, shard_min=1))
+        assert g2.distance == base.distance
+    finally:
+        comm.close()

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 15
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.sdb_abi_version() == 1
+    assert lib.sdb_abi_version() == 2
     # the Python mirror binds exactly the header's symbols
     assert set(P._EXPORTS) == set(syms)
 
