@@ -135,6 +135,7 @@ SDB_HD inline TileSmem tile_smem_layout(int G, int N, int W, int BK) {
 
 struct TilePlan {
     int g, t, h;
+    int tchunk;                     // tails per unit (<= kTailChunk; smaller for mid-size levels)
     unsigned int thr0;              // candidates with weight <= thr0 are considered (U - 1)
     int nb;                         // number of boundaries b in [h, N - t]
     const unsigned long long *cum;  // [G * nb + 1] cumulative unit counts over (j, b)

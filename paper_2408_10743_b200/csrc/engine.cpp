@@ -400,34 +400,52 @@ cudaEvent_t Plan::level_event(int i) {
 
 size_t tile_smem_bytes(int G, int N, int W, int SW, int BK);
 
-int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel) {
-    if (forced_kernel == 1 || g < 2) return 0;
-    const double HBk = head_block(W), Hl = heads_per_lane(W);
+TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms) {
+    TileChoice best{0, kTailChunk};
+    if (forced_kernel == 1 || g < 2) return best;
     const double total = double(per_gamma) * G;
-    if (forced_kernel != 2 && total < double(1 << 22)) return 0;
-    // relative lane-cycle costs: walk ~12 per candidate; tile ~1 per candidate plus
-    // per-unit head generation (unrank + successors), tail staging and scheduling
-    const double walk_cost = total * 12.0;
-    double best = 0;
-    int best_t = 0;
+    if (forced_kernel != 2 && total < double(1 << 16)) return best;
+    // Level time in candidate-equivalents per CTA slot: max(total load / slots, the largest
+    // unit) — a level with few big units is bound by its slowest CTA. A tile unit costs its
+    // padded candidates (every lane of a warp with heads runs H heads) plus ~20k for the
+    // dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
+    // (measured 1.4e11 vs 3.9e12 cand/s) with perfectly fine granularity.
+    const double Hl = heads_per_lane(W), HBk = head_block(W);
+    const double slots = double(num_sms) * tile_blocks_per_sm(W);
+    std::vector<double> C(size_t(N + 1) * size_t(N + 1), 0.0);  // Pascal's triangle in doubles
+    for (int a = 0; a <= N; a++)
+        for (int k = 0; k <= a; k++)
+            C[size_t(a) * (N + 1) + size_t(k)] =
+                (k == 0 || k == a) ? 1.0 : C[size_t(a - 1) * (N + 1) + size_t(k - 1)] + C[size_t(a - 1) * (N + 1) + size_t(k)];
+    double best_time = total * 28.0 / slots;
+    if (forced_kernel == 2) best_time = 1e300;
     for (int t = 1; t < g; t++) {
         const int h = g - t;
-        double cost = 0;
-        for (int b = h; b <= N - t; b++) {
-            const double Hb = double(binom_u64(b, h)), Tb = double(binom_u64(N - 1 - b, t - 1));
-            const double nH = std::ceil(Hb / HBk), nT = std::ceil(Tb / kTailChunk);
-            const double tc = Tb / nT;
-            const double heads_last = Hb - (nH - 1) * HBk;
-            const double warps_full = kTileThreads / 32, warps_last = std::ceil(heads_last / (32.0 * Hl));
-            const double warps = ((nH - 1) * warps_full + warps_last) / nH;
-            const double unit = 32.0 * (warps * (Hl * tc + 100.0) + warps_full * (0.2 * tc + 60.0));
-            cost += nH * nT * unit;
+        for (int tchunk = kTailChunk; tchunk >= 64; tchunk /= 2) {
+            double sum = 0, biggest = 0;
+            for (int b = h; b <= N - t; b++) {
+                const double Hb = C[size_t(b) * (N + 1) + size_t(h)], Tb = C[size_t(N - 1 - b) * (N + 1) + size_t(t - 1)];
+                const double nH = std::ceil(Hb / HBk), nT = std::ceil(Tb / tchunk);
+                const double heads_last = Hb - (nH - 1) * HBk;
+                const double warps_full = kTileThreads / 32.0, warps_last = std::ceil(heads_last / (32.0 * Hl));
+                const double tc = Tb / nT;  // average tails per unit
+                const double unit_full = warps_full * 32 * Hl * tc + 20000, unit_last = warps_last * 32 * Hl * tc + 20000;
+                sum += nT * ((nH - 1) * unit_full + unit_last);
+                biggest = std::max(biggest, nH > 1 ? unit_full : unit_last);
+            }
+            sum *= G;
+            const double time = std::max(sum / slots, biggest);
+            if (time < best_time) {
+                best_time = time;
+                best = TileChoice{t, tchunk};
+            }
         }
-        cost *= G;
-        if (best_t == 0 || cost < best) { best = cost; best_t = t; }
     }
-    if (forced_kernel == 2) return best_t;
-    return best < walk_cost ? best_t : 0;
+    return best;
+}
+
+int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel) {
+    return choose_tile(G, N, g, W, per_gamma, forced_kernel, 148).t;
 }
 
 long long Plan::lower_bound(int g) const {
@@ -477,7 +495,7 @@ void Plan::prepare_level(int g) {
             total += L.total[j];
         }
         const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
-        L.seg_len = std::max<unsigned long long>(64, (total + threads_total * 4 - 1) / (threads_total * 4));
+        L.seg_len = std::max<unsigned long long>(1, (total + threads_total - 1) / threads_total);
         L.seg_total = 0;
         for (int j = 0; j < G_; j++) {
             L.segs[j] = (L.total[j] + L.seg_len - 1) / L.seg_len;
@@ -492,15 +510,17 @@ void Plan::prepare_level(int g) {
     const unsigned long long per = binom_u64(N_, g);
     if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
     const unsigned long long total = per * (unsigned long long)G_;
-    lv.t = choose_tile_t(G_, N_, g, W_, per, opts_.kernel);
+    const TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_);
+    lv.t = tc.t;
     if (lv.t == 0) {
         LevelLaunch &LL = lv.walk;
         LL.g = g;
         LL.thr0 = ~0u;  // the kernels read U from the device (RunCtl)
         LL.per_gamma = per;
         const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
-        const unsigned long long seg = (total + threads_total * 4 - 1) / (threads_total * 4);
-        LL.seg_len = std::max<unsigned long long>(64, seg);
+        // one segment per thread of the full grid: tiny levels get one candidate per thread
+        // instead of a long serial walk on a few threads
+        LL.seg_len = std::max<unsigned long long>(1, (total + threads_total - 1) / threads_total);
         LL.segs_per_gamma = (per + LL.seg_len - 1) / LL.seg_len;
         const unsigned long long S = LL.segs_per_gamma * (unsigned long long)G_;
         LL.seg_total = S;
@@ -513,6 +533,7 @@ void Plan::prepare_level(int g) {
         tp.h = g - lv.t;
         tp.thr0 = ~0u;
         tp.nb = N_ - lv.t - tp.h + 1;
+        tp.tchunk = tc.tchunk;
         tp.per_gamma = per;
         const size_t n_entries = size_t(G_) * size_t(tp.nb) + 1;
         if (table_used_ + n_entries > table_cap_) throw InternalFailure("tile unit tables overflow");
@@ -522,7 +543,7 @@ void Plan::prepare_level(int g) {
             for (int b = tp.h; b <= N_ - lv.t; b++) {
                 h_table_[size_t(j) * tp.nb + (b - tp.h)] = acc;
                 const unsigned long long Hb = binom_u64(b, tp.h), Tb = binom_u64(N_ - 1 - b, lv.t - 1);
-                acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + kTailChunk - 1) / kTailChunk);
+                acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
             }
         h_table_[size_t(G_) * tp.nb] = acc;
         tp.unit_total = acc;

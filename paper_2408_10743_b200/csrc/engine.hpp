@@ -108,6 +108,11 @@ class Plan {
 
 // Host cost model for one level: 0 = lexicographic-walk kernel, else the tail size t of
 // the head x tail tile kernel. Exposed for tests.
+struct TileChoice {
+    int t;       // 0: walk kernel
+    int tchunk;  // tails per unit
+};
+TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms);
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel);
 
 // Per Gamma and 32-symbol block, swap the x- and z-words of every row so that the word the

@@ -599,12 +599,12 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
                 const unsigned long long u = unit - __ldg(tp.cum + lo);
                 const unsigned long long Hb = binom_at(s_binom, p.BK, b, tp.h);
                 const unsigned long long Tb = binom_at(s_binom, p.BK, N - 1 - b, tp.t - 1);
-                const unsigned long long nT = (Tb + kTailChunk - 1) / kTailChunk;
+                const unsigned long long nT = (Tb + tp.tchunk - 1) / tp.tchunk;
                 const unsigned long long hc = u / nT, tc = u % nT;
                 s_un.j = lo / tp.nb;
                 s_un.b = b;
-                s_un.t0 = tc * kTailChunk;
-                s_un.tcount = int(min((unsigned long long)kTailChunk, Tb - s_un.t0));
+                s_un.t0 = tc * tp.tchunk;
+                s_un.tcount = int(min((unsigned long long)tp.tchunk, Tb - s_un.t0));
                 s_un.hbase0 = hc * HB;
                 s_un.pad = int(min((unsigned long long)HB, Hb - hc * HB));  // heads in this block
                 s_visited += (unsigned long long)s_un.pad * (unsigned long long)s_un.tcount;
