@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -89,9 +91,16 @@ void saved_isometry_impl(const uint64_t *rows, int n_rows, int n_cols, int row_w
     if (f.enabled) f.rows = a;
     const auto tp = std::chrono::steady_clock::now();
     sdb::Plan plan(std::move(gammas), sdb::Mode::hamming, n, f, o);
+    const auto tq = std::chrono::steady_clock::now();
     rep->h2d_bytes = plan.upload_bytes;
     plan.run(rep, trace, trace_cap, best_out, nullptr);
     rep->prep_seconds = std::chrono::duration<double>(tp - t0).count() + plan.h2d_seconds;
+    if (std::getenv("SDB_TRACE_HOST"))
+        std::fprintf(stderr, "[sdb] prep %.3f ms, plan %.3f ms, run %.3f ms (levels %.3f ms)\n",
+                     1e3 * std::chrono::duration<double>(tp - t0).count(),
+                     1e3 * std::chrono::duration<double>(tq - tp).count(),
+                     1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tq).count(),
+                     1e3 * rep->enum_seconds);
     if (rep->complete && rep->upper % 2 != 0)
         throw sdb::InternalFailure("saved_isometry: image Hamming distance must be even");
     rep->distance = int(rep->upper / 2);

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <mutex>
@@ -99,9 +101,10 @@ int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, 
     std::vector<uint64_t> proj(size_t((2 * n + 63) / 64));
     for (int j = 0; j < G; j++)
         for (int i = 0; i < gammas[size_t(j)].matrix.rows; i++) {
-            std::fill(proj.begin(), proj.end(), 0);
-            for (int c = 0; c < 2 * n; c++)
-                if (gammas[size_t(j)].matrix.get(i, c)) proj[size_t(c >> 6)] |= uint64_t(1) << (c & 63);
+            // first 2n columns of the row (the reference's projection, engine.cpp:168-173)
+            const uint64_t *src = gammas[size_t(j)].matrix.row(i);
+            for (size_t w = 0; w < proj.size(); w++) proj[w] = src[w];
+            if ((2 * n) & 63) proj.back() &= (uint64_t(1) << ((2 * n) & 63)) - 1;
             for (int r = 0; r < F; r++)
                 if (symplectic_ip(proj.data(), f.rows.row(r), n)) S.set(j * N + i, r, true);
         }
@@ -185,6 +188,14 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
     }
     if (W_ < 1) W_ = 1;
     if (W_ > kMaxW) throw InvalidArgument("rows too wide for the enumeration kernels (n > 256)");
+    const bool trace_host = std::getenv("SDB_TRACE_HOST") != nullptr;
+    auto tick = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (!trace_host) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[sdb]   plan %s %.3f ms\n", what, 1e3 * std::chrono::duration<double>(now - tick).count());
+        tick = now;
+    };
     h_rows_.assign(size_t(G_) * N_ * 2 * W_, 0);
     for (int j = 0; j < G_; j++)
         for (int r = 0; r < gammas_[size_t(j)].matrix.rows; r++) {
@@ -197,10 +208,14 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
                 extract_bits(m, r, 0, cols, dst, W_);
             }
         }
+    lap("rows");
     if (!packaged_) orient_probe_words(h_rows_, G_, N_, W_);
+    lap("orient");
     SW_ = build_syndromes(gammas_, n, filter, h_syn_);
+    lap("syndromes");
     BK_ = std::min(N_, kMaxLevel) + 2;
     h_binom_ = binom_table(N_, BK_);
+    lap("binom");
     if (packaged_) {
         // package tables and weighted suffix counts wsuf(q, m) = wsuf(q+1, m) + s_q wsuf(q+1, m-1)
         const unsigned long long cap = 1ull << 62;
@@ -226,6 +241,7 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
         }
     }
     upload();
+    lap("upload");
 }
 
 // ---- process-wide caches: repeated distance calls skip cudaMalloc / stream / event creation
@@ -289,6 +305,32 @@ void event_put(int device, cudaEvent_t e) {
     g_free_events.emplace_back(device, e);
 }
 
+std::vector<std::pair<size_t, void *>> g_free_pinned;
+
+void *pinned_get(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_free_pinned.size(); i++)
+            if (g_free_pinned[i].first >= bytes && g_free_pinned[i].first <= 4 * bytes + (1 << 20)) {
+                void *p = g_free_pinned[i].second;
+                g_free_pinned.erase(g_free_pinned.begin() + long(i));
+                return p;
+            }
+    }
+    void *p = nullptr;
+    check_cuda(cudaMallocHost(&p, bytes), "cudaMallocHost");
+    return p;
+}
+
+void pinned_put(size_t bytes, void *p) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_free_pinned.emplace_back(bytes, p);
+    if (g_free_pinned.size() > 16) {
+        cudaFreeHost(g_free_pinned.front().second);
+        g_free_pinned.erase(g_free_pinned.begin());
+    }
+}
+
 // one non-blocking stream per (thread, device), kept for the process lifetime
 cudaStream_t thread_stream(int device) {
     thread_local std::vector<std::pair<int, cudaStream_t>> streams;
@@ -302,10 +344,9 @@ cudaStream_t thread_stream(int device) {
 }  // namespace
 
 Plan::~Plan() {
-    if (d_mem_) {
-        cudaStreamSynchronize(stream_);
-        workspace_put(device_, d_bytes_, d_mem_);
-    }
+    if (d_mem_ || h_pinned_) cudaStreamSynchronize(stream_);
+    if (d_mem_) workspace_put(device_, d_bytes_, d_mem_);
+    if (h_pinned_) pinned_put(table_cap_ * 8, h_pinned_);
     for (cudaEvent_t e : events_)
         if (e) event_put(device_, e);
 }
@@ -355,6 +396,7 @@ void Plan::upload() {
     d_counter_init_ = reinterpret_cast<unsigned long long *>(q);
     q += b_counters;
     d_tables_ = reinterpret_cast<unsigned long long *>(q);
+    h_pinned_ = static_cast<unsigned long long *>(pinned_get(table_cap_ * 8));
     q += b_tables;
     if (packaged_) {
         pk_.pk_rows = reinterpret_cast<const short *>(q);
@@ -400,7 +442,8 @@ cudaEvent_t Plan::level_event(int i) {
 
 size_t tile_smem_bytes(int G, int N, int W, int SW, int BK);
 
-TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms) {
+TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
+                       int world) {
     TileChoice best{0, kTailChunk};
     if (forced_kernel == 1 || g < 2) return best;
     const double total = double(per_gamma) * G;
@@ -411,7 +454,7 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
     // dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
     // (measured 1.4e11 vs 3.9e12 cand/s) with perfectly fine granularity.
     const double Hl = heads_per_lane(W), HBk = head_block(W);
-    const double slots = double(num_sms) * tile_blocks_per_sm(W);
+    const double slots = double(num_sms) * tile_blocks_per_sm(W) * std::max(1, world);  // all ranks' CTAs
     std::vector<double> C(size_t(N + 1) * size_t(N + 1), 0.0);  // Pascal's triangle in doubles
     for (int a = 0; a <= N; a++)
         for (int k = 0; k <= a; k++)
@@ -445,7 +488,7 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
 }
 
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel) {
-    return choose_tile(G, N, g, W, per_gamma, forced_kernel, 148).t;
+    return choose_tile(G, N, g, W, per_gamma, forced_kernel, 148, 1).t;
 }
 
 long long Plan::lower_bound(int g) const {
@@ -477,7 +520,7 @@ void Plan::prepare_level(int g) {
     LevelHost &lv = levels_[size_t(g)];
     if (lv.ready) return;
     // small levels run whole on every rank (identical results, no exchange); big ones shard
-    const unsigned long long shard_min = opts_.shard_min > 0 ? (unsigned long long)opts_.shard_min : (1ull << 30);
+    const unsigned long long shard_min = opts_.shard_min > 0 ? (unsigned long long)opts_.shard_min : kDefaultShardMin;
     // (a one-rank communicator with shard_min = 1 takes the exchange path too: the single-GPU
     // test of the NCCL plumbing)
     lv.sharded = (opts_.world > 1 || (opts_.comm && opts_.shard_min == 1)) && level_candidates(g) >= shard_min;
@@ -510,7 +553,7 @@ void Plan::prepare_level(int g) {
     const unsigned long long per = binom_u64(N_, g);
     if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
     const unsigned long long total = per * (unsigned long long)G_;
-    const TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_);
+    const TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_, world);
     lv.t = tc.t;
     if (lv.t == 0) {
         LevelLaunch &LL = lv.walk;
@@ -537,31 +580,25 @@ void Plan::prepare_level(int g) {
         tp.per_gamma = per;
         const size_t n_entries = size_t(G_) * size_t(tp.nb) + 1;
         if (table_used_ + n_entries > table_cap_) throw InternalFailure("tile unit tables overflow");
-        h_table_.resize(n_entries);
+        // staged in the plan's pinned buffer: the copy is truly asynchronous, no wait here
+        unsigned long long *h_table = h_pinned_ + table_used_;
         unsigned long long acc = 0;
         for (int j = 0; j < G_; j++)
             for (int b = tp.h; b <= N_ - lv.t; b++) {
-                h_table_[size_t(j) * tp.nb + (b - tp.h)] = acc;
+                h_table[size_t(j) * tp.nb + (b - tp.h)] = acc;
                 const unsigned long long Hb = binom_u64(b, tp.h), Tb = binom_u64(N_ - 1 - b, lv.t - 1);
                 acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
             }
-        h_table_[size_t(G_) * tp.nb] = acc;
+        h_table[size_t(G_) * tp.nb] = acc;
         tp.unit_total = acc;
         tp.shard_rank = rank;
         tp.shard_world = world;
         tp.cum = d_tables_ + table_used_;
-        tp.counter = d_counters_ + g;
+        tp.counter = d_counters_ + g;  // zeroed by run_init at the start of every run
         table_used_ += n_entries;
-        h_counter_init_[size_t(g)] = 0;
-        // pageable sources: the copies are staged before cudaMemcpyAsync returns
-        check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table_.data(), n_entries * 8,
+        check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table, n_entries * 8,
                                    cudaMemcpyHostToDevice, stream_),
                    "H2D unit table");
-        check_cuda(cudaMemcpyAsync(d_counter_init_ + g, &h_counter_init_[size_t(g)], 8, cudaMemcpyHostToDevice, stream_),
-                   "H2D unit counter");
-        check_cuda(cudaMemcpyAsync(d_counters_ + g, &h_counter_init_[size_t(g)], 8, cudaMemcpyHostToDevice, stream_),
-                   "H2D unit counter");
-        check_cuda(cudaStreamSynchronize(stream_), "H2D unit table sync");
         if (tile_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
             throw InvalidArgument("problem too large for shared-memory staging");
     }

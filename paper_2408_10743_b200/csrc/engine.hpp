@@ -93,7 +93,8 @@ class Plan {
     unsigned long long *d_counter_init_ = nullptr;
     unsigned long long *d_tables_ = nullptr;    // tile unit tables of all levels, back to back
     size_t table_cap_ = 0, table_used_ = 0;
-    std::vector<unsigned long long> h_counter_init_, h_table_;
+    std::vector<unsigned long long> h_counter_init_;
+    unsigned long long *h_pinned_ = nullptr;  // pinned staging of the unit tables (table_cap_ entries)
     // package routes
     bool packaged_ = false;
     int P_ = 0;                                  // package slots per Gamma
@@ -112,7 +113,10 @@ struct TileChoice {
     int t;       // 0: walk kernel
     int tchunk;  // tails per unit
 };
-TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms);
+TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
+                       int world);
+// levels with fewer candidates run whole on every rank (RunOptions.shard_min = 0)
+constexpr unsigned long long kDefaultShardMin = 1ull << 24;
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel);
 
 // Per Gamma and 32-symbol block, swap the x- and z-words of every row so that the word the

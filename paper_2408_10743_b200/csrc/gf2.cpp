@@ -166,13 +166,25 @@ static uint64_t xorshift64star(uint64_t &s) {
     return s * 0x2545F4914F6CDD1DULL;
 }
 
+// bits [from, from + 64) of a packed row (zero beyond the row's words is the caller's padding)
+static inline uint64_t word_at(const uint64_t *r, int from) {
+    const int wi = from >> 6, sh = from & 63;
+    return sh ? (r[wi] >> sh) | (r[wi + 1] << (64 - sh)) : r[wi];
+}
+
 int symplectic_ip(const uint64_t *u, const uint64_t *v, int n) {
-    // bits [0,n) are x, [n,2n) are z
+    // bits [0, n) are x, [n, 2n) are z: parity of popc(u_x & v_z) + popc(u_z & v_x), 64 at a time
     int par = 0;
-    for (int i = 0; i < n; i++) {
-        const int xi = int((u[i >> 6] >> (i & 63)) & 1u), zi = int((u[(n + i) >> 6] >> ((n + i) & 63)) & 1u);
-        const int vx = int((v[i >> 6] >> (i & 63)) & 1u), vz = int((v[(n + i) >> 6] >> ((n + i) & 63)) & 1u);
-        par ^= (xi & vz) ^ (zi & vx);
+    for (int i = 0; i < n; i += 64) {
+        const int len = std::min(64, n - i);
+        const uint64_t mask = len == 64 ? ~uint64_t(0) : ((uint64_t(1) << len) - 1);
+        // word_at may read one word past the x block; row strides cover 2n bits, and the
+        // z block lies right after, so reads stay inside the row
+        const uint64_t ux = word_at(u, i) & mask, uz = (((n + i) & 63) + len > 64 || len == 64 ? word_at(u, n + i)
+                                                                                                : u[(n + i) >> 6] >> ((n + i) & 63)) & mask;
+        const uint64_t vx = word_at(v, i) & mask, vz = (((n + i) & 63) + len > 64 || len == 64 ? word_at(v, n + i)
+                                                                                                : v[(n + i) >> 6] >> ((n + i) & 63)) & mask;
+        par ^= (__builtin_popcountll(ux & vz) ^ __builtin_popcountll(uz & vx)) & 1;
     }
     return par;
 }
