@@ -95,7 +95,10 @@ int launch_walk_level(const ProblemDev &p, const LevelLaunch &L, void *stream, i
 // the CTA stages the tail chunk in shared memory, each lane holds heads_per_lane(W) heads in
 // registers and streams the tails as warp-uniform broadcast loads, so one candidate is
 // one XOR of two precomputed sums fused with the OR (2 LOP3) plus one POPC.
-constexpr int kTileThreads = 256;
+#ifndef SDB_TILE_THREADS
+#define SDB_TILE_THREADS 256
+#endif
+constexpr int kTileThreads = SDB_TILE_THREADS;
 // heads held in registers per lane (2W words each); fewer for wide rows to avoid spills
 #ifndef SDB_HEADS_W2
 #define SDB_HEADS_W2 8
@@ -114,7 +117,9 @@ constexpr int kTailChunk = SDB_TAIL_CHUNK;
 #ifndef SDB_TILE_BLOCKS
 #define SDB_TILE_BLOCKS 3
 #endif
-SDB_HD constexpr int tile_blocks_per_sm(int W) { return W <= 2 ? SDB_TILE_BLOCKS_W2 : SDB_TILE_BLOCKS; }
+SDB_HD constexpr int tile_blocks_per_sm(int W) {
+    return (W <= 2 ? SDB_TILE_BLOCKS_W2 : SDB_TILE_BLOCKS) * (256 / kTileThreads);
+}
 // Staged tail chunk: the probe words of each tail, [kTailChunk+1][probe_stride(W)] (W = 1
 // keeps both words of its single symbol block there: its fast path is exact). probe_stride
 // is even so two tails are whole 16-byte loads. The rare exact path rebuilds candidates

@@ -599,7 +599,7 @@ void Plan::prepare_level(int g) {
         check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table, n_entries * 8,
                                    cudaMemcpyHostToDevice, stream_),
                    "H2D unit table");
-        if (tile_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
+        if (tile_smem_bytes(G_, N_, W_, SW_, std::min(BK_, g + 2)) > 200 * 1024)
             throw InvalidArgument("problem too large for shared-memory staging");
     }
     lv.ready = true;

@@ -492,14 +492,14 @@ struct TileUnit {
 // engine.cpp:14-29) and publishes (weight, key). Returns the updated threshold.
 template <int W>
 __device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan tp, const uint32_t *s_rows,
-                                            const unsigned long long *s_binom, const TileUnit *un, int head_off,
-                                            int tix, unsigned thrH) {
+                                            const unsigned long long *s_binom, int BKs, const TileUnit *un,
+                                            int head_off, int tix, unsigned thrH) {
     const int N = p.N, h = tp.h, t = tp.t, g = tp.g, j = un->j, b = un->b;
     const uint32_t *grows = s_rows + j * N * 2 * W;
     int c[kMaxLevel];
-    unrank_colex(un->hbase0 + head_off, h, b, s_binom, p.BK, c);
+    unrank_colex(un->hbase0 + head_off, h, b, s_binom, BKs, c);
     c[h] = b;
-    unrank_colex(un->t0 + tix, t - 1, N - 1 - b, s_binom, p.BK, c + h + 1);
+    unrank_colex(un->t0 + tix, t - 1, N - 1 - b, s_binom, BKs, c + h + 1);
     for (int k = h + 1; k < g; k++) c[k] += b + 1;
     uint32_t acc[2 * W];
 #pragma unroll
@@ -518,7 +518,7 @@ __device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan t
         if (!adm) return thrH;
     }
     const unsigned long long key =
-        ((unsigned long long)j << kKeyRankBits) | lexrank(c, g, N, s_binom, p.BK, tp.per_gamma);
+        ((unsigned long long)j << kKeyRankBits) | lexrank(c, g, N, s_binom, BKs, tp.per_gamma);
     atomicMin(&p.state->wmin, wv);
     atomicMin(&p.key_by_w[wv], key);
     return wv;
@@ -568,16 +568,19 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowlen = 2 * W;
     const int G = p.G, N = p.N;
-    const TileSmem lay = tile_smem_layout(G, N, W, p.BK);
+    // binomials C(a, k) for k <= g + 1 only: the level needs no wider ones, and the slice keeps
+    // shared memory small enough for many resident CTAs
+    const int BKs = min(p.BK, tp.g + 2);
+    const TileSmem lay = tile_smem_layout(G, N, W, BKs);
     const int nrow_words = G * N * rowlen;
     uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem + lay.rows);
     unsigned long long *s_binom = reinterpret_cast<unsigned long long *>(smem + lay.binom);
-    const int nbinom = (N + 1) * p.BK;
+    const int nbinom = (N + 1) * BKs;
     uint32_t *s_tp = reinterpret_cast<uint32_t *>(smem + lay.tp);
     __shared__ TileUnit s_un;
     __shared__ unsigned long long s_visited;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
-    for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[i];
+    for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
     if (threadIdx.x == 0) s_visited = 0;
 
     const unsigned sshift = p.scale == 2 ? 1u : 0u;
@@ -597,8 +600,8 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
                 }
                 const int b = tp.h + lo % tp.nb;
                 const unsigned long long u = unit - __ldg(tp.cum + lo);
-                const unsigned long long Hb = binom_at(s_binom, p.BK, b, tp.h);
-                const unsigned long long Tb = binom_at(s_binom, p.BK, N - 1 - b, tp.t - 1);
+                const unsigned long long Hb = binom_at(s_binom, BKs, b, tp.h);
+                const unsigned long long Tb = binom_at(s_binom, BKs, N - 1 - b, tp.t - 1);
                 const unsigned long long nT = (Tb + tp.tchunk - 1) / tp.tchunk;
                 const unsigned long long hc = u / nT, tc = u % nT;
                 s_un.j = lo / tp.nb;
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
             const int i0 = threadIdx.x * R, i1 = min(i0 + R, tcount);
             if (i0 < i1) {
                 int e[kMaxLevel];
-                unrank_colex(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, p.BK, e);
+                unrank_colex(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, BKs, e);
                 uint32_t acc[NW];
 #pragma unroll
                 for (int w = 0; w < NW; w++) acc[w] = grows[b * rowlen + w];
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
             int e[kMaxLevel];
             uint32_t acc[NW];
             if (nvalid > 0) {
-                unrank_colex(s_un.hbase0 + lane_head, h, b, s_binom, p.BK, e);
+                unrank_colex(s_un.hbase0 + lane_head, h, b, s_binom, BKs, e);
 #pragma unroll
                 for (int w = 0; w < NW; w++) acc[w] = 0;
                 for (int k = 0; k < h; k++)
@@ -713,7 +716,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
             while (fire) {
                 const int k = __ffs(fire) - 1;
                 fire &= fire - 1;
-                thrH = tile_exact<W>(p, tp, s_rows, s_binom, &s_un, lane_head + (k >> 1), ti + (k & 1), thrH);
+                thrH = tile_exact<W>(p, tp, s_rows, s_binom, BKs, &s_un, lane_head + (k >> 1), ti + (k & 1), thrH);
             }
             thr0 = thrH >> sshift;
             ti += 2;
@@ -727,7 +730,7 @@ size_t tile_smem(int G, int N, int W, int SW, int BK) { (void)SW; return tile_sm
 
 template <int W>
 int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, int num_sms) {
-    const size_t smem = tile_smem(p.G, p.N, W, p.SW, p.BK);
+    const size_t smem = tile_smem(p.G, p.N, W, p.SW, min(p.BK, tp.g + 2));
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -215,6 +215,18 @@ def package_routes(heavy: bool, workers: int) -> dict:
     return dict(cases=cases, config3_auto=dict(n=c["n"], k=c["k"], codes=batch))
 
 
+def wide_codes() -> dict:
+    """Wide rows (n up to 256: 4-8 u32 words per half, the kernels' upper limit) through the
+    first levels of saved_isometry, answered by the reference (levels g <= g_max)."""
+    cases = []
+    for n, k, g in [(100, 5, 4), (130, 7, 3), (160, 0, 3), (200, 10, 2), (256, 0, 2), (256, 12, 2)]:
+        a = O.generate(n, k, 11)
+        lv = O.ref_isometry_levels(a, workers=os.cpu_count() or 1, g_max=g, native=True)
+        cases.append(dict(n=n, k=k, seed=11, g_max=g, normalizer=hexrows(a), trace=lv["trace"],
+                          level_candidates=lv["level_candidates"]))
+    return dict(cases=cases)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true", help="also config 4 (full) and config 5 (g<=8)")
@@ -236,6 +248,8 @@ def main() -> None:
         dump("reference_kats.json", reference_kats())
     if want("engine"):
         dump("engine_kats.json", engine_kats())
+    if want("wide"):
+        dump("wide_codes.json", wide_codes())
     if want("packages"):
         dump("package_routes.json", package_routes(args.heavy, args.workers))
     if args.heavy and want("c4"):

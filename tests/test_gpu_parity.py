@@ -235,3 +235,30 @@ def test_batch_device_prep_shapes(gpu, nk):
     host = gpu.saved_isometry_batch(codes, gpu.RunOptions(kernel=3, max_generation=3 if n > 40 else 0))
     assert (dev.statuses == host.statuses).all()
     assert dev.traces == host.traces
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 2])
+def test_wide_rows_first_levels(gpu, kernel):
+    # n up to 256 (W = 4..8 words per half, the kernels' limit): the reference's first levels
+    gd = load_golden("wide_codes.json")
+    for case in gd["cases"]:
+        a = hex_to_mat(case["normalizer"], 2 * case["n"])
+        rep = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel, max_generation=case["g_max"]))
+        assert tr(rep) == [tuple(t) for t in case["trace"]], (case["n"], case["k"], kernel)
+        assert rep.candidates_enumerated == sum(case["level_candidates"])
+        assert rep.candidates_visited == rep.candidates_enumerated
+
+
+def test_edge_shapes(gpu):
+    # n = 1 codes, k = n (no stabilizer), k = 0, a single row, rows exactly on a word boundary
+    for n, k in [(1, 0), (1, 1), (2, 2), (32, 0), (32, 1), (64, 0), (31, 1), (33, 2)]:
+        a = gpu.generate_code(n, k, 5)
+        rep = gpu.saved_isometry(a, gpu.RunOptions(max_generation=4))
+        ref = O.run_levels(a, g_max=4)
+        assert tr(rep) == ref["trace"], (n, k)
+    with pytest.raises(gpu.ValidationError):  # validate_normalizer: "matrix has no rows"
+        gpu.saved_isometry(np.zeros((0, 4), dtype=np.uint8))
+    with pytest.raises(ValueError):
+        gpu.saved_isometry(np.zeros((2, 3), dtype=np.uint8))  # odd column count
+    with pytest.raises(ValueError):
+        gpu.saved_isometry_batch([])

@@ -91,7 +91,7 @@ def test_small_levels_run_whole_on_every_rank(gpu):
         calls.append(1)
         return v
 
-    rep = gpu.saved_isometry(a, gpu.RunOptions(rank=1, world=2, allreduce_min=never))
+    rep = gpu.saved_isometry(a, gpu.RunOptions(rank=1, world=2, allreduce_min=never, shard_min=1 << 40))
     assert tr(rep) == tr(single) and not calls
     assert rep.candidates_visited == single.candidates_visited
 
