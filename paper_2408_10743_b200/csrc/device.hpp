@@ -60,6 +60,8 @@ struct ProblemDev {
     unsigned long long *key_by_w;
     RunCtl *ctl;
     int *trace_upper;               // [N + 1]: U after level g (-1: level skipped)
+    const uint32_t *prows;          // [G][N][K] the tile kernels' probe words of every row
+    int K;                          // probe words per row (W, W + 1 with an extra probe, 2 when W = 1)
     int G, N, W, SW, BK;
     int scale;
     int max_weight;
@@ -120,21 +122,22 @@ constexpr int kTailChunk = SDB_TAIL_CHUNK;
 SDB_HD constexpr int tile_blocks_per_sm(int W) {
     return (W <= 2 ? SDB_TILE_BLOCKS_W2 : SDB_TILE_BLOCKS) * (256 / kTileThreads);
 }
-// Staged tail chunk: the probe words of each tail, [kTailChunk+1][probe_stride(W)] (W = 1
-// keeps both words of its single symbol block there: its fast path is exact). probe_stride
-// is even so two tails are whole 16-byte loads. The rare exact path rebuilds candidates
-// from the rows, so nothing else is staged per tail.
-SDB_HD constexpr int probe_stride(int W) { return W == 1 ? 2 : (W + 1) & ~1; }
+// Staged tail chunk: the probe words of each tail, [kTailChunk+1][probe_stride(K)] with K =
+// probe words per row (ProblemDev.prows). probe_stride is even so two tails are whole 16-byte
+// loads. The rare exact path rebuilds candidates from the full rows, so nothing else is
+// staged per tail.
+SDB_HD constexpr int probe_stride(int K) { return (K + 1) & ~1; }
 SDB_HD constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 struct TileSmem {
-    size_t rows, binom, tp, total;
+    size_t rows, prows, binom, tp, total;
 };
-SDB_HD inline TileSmem tile_smem_layout(int G, int N, int W, int BK) {
+SDB_HD inline TileSmem tile_smem_layout(int G, int N, int W, int K, int BK) {
     TileSmem L{};
     L.rows = 0;
-    L.binom = align16(size_t(G) * N * 2 * W * 4);
+    L.prows = align16(size_t(G) * N * 2 * W * 4);
+    L.binom = align16(L.prows + size_t(G) * N * K * 4);
     L.tp = align16(L.binom + size_t(N + 1) * BK * 8);
-    L.total = align16(L.tp + size_t(kTailChunk + 1) * probe_stride(W) * 4);
+    L.total = align16(L.tp + size_t(kTailChunk + 1) * probe_stride(K) * 4);
     return L;
 }
 
@@ -178,6 +181,34 @@ struct PkgLevel {
     int shard_rank, shard_world;
 };
 size_t pkg_smem_bytes(int G, int N, int W, int SW, int P, int BK);
+
+// Packaged head x tail tile kernel (ptile_kernel<W>). A package member is an "element"
+// e = off(q) + m of Gamma j; a candidate is a set of g elements from distinct packages.
+// Element sets are enumerated in colex order with weighted counts
+//   F(x, i) = number of i-element sets with distinct packages inside elements [0, x)
+//           = F(x-1, i) + F(off(pkg(x-1)), i-1),
+// forward for heads (packages < b) and over the reversed package order for tails (packages
+// > b), so heads and tails unrank and step exactly like the singleton tile kernel.
+struct PtileDev {
+    const short *e_row, *e_pkg;          // [G][E] forward: row / package of element e
+    const short *r_row, *r_pkg;          // [G][E] reversed package order
+    const short *off, *r_off;            // [G][P + 1] first element of package q
+    const unsigned long long *F, *FR;    // [G][E + 1][BK]
+    int E;                               // element slots per Gamma
+};
+struct PTilePlan {
+    int g, t, h, tchunk;
+    unsigned int thr0;
+    int npairs;                          // (Gamma, b) pairs with work
+    const unsigned long long *cum;       // [npairs + 1] cumulative unit counts
+    const unsigned int *pairs;           // [npairs] j << 16 | b
+    unsigned long long *counter;
+    unsigned long long unit_total;
+    int shard_rank, shard_world;
+};
+size_t ptile_smem_bytes(int G, int N, int W, int K, int P, int E, int BKs);
+int launch_ptile_level(const ProblemDev &p, const PkgDev &k, const PtileDev &d, const PTilePlan &tp, void *stream,
+                       int num_sms);
 int launch_pkg_level(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, void *stream, int num_sms);
 
 // Brute force (reference brute_force_distance, distance.cpp:151-224): the Gray-code walk over

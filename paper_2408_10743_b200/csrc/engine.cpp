@@ -54,13 +54,15 @@ static void extract_bits(const BitMat &m, int r, int from, int len, uint32_t *ds
         if (m.get(r, from + c)) dst[c >> 5] |= 1u << (c & 31);
 }
 
-void orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
+ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
     // popc(x|z) is symmetric in x and z position by position, so swapping the x-word and
     // the z-word of one 32-symbol block (in every row of a Gamma) leaves every candidate
-    // weight unchanged. The tile kernel's fast path folds only the first (probe) word of
-    // each block, so put the component that is denser in sums of rows there: systematic
-    // Gamma_j carry an identity block in one component (the x columns of Gamma_1 on the
-    // isometry route), which makes that component sparse in every combination.
+    // weight unchanged. The tile kernels' fast path folds the first (probe) word of each
+    // block, so put the component that is denser in sums of rows there: systematic Gamma_j
+    // carry an identity block in one component (the x columns of Gamma_1 on the isometry
+    // route), which makes that component sparse in every combination. When even the
+    // oriented probe words fold sparse (pivot-heavy blocks, e.g. the F4-diagonalized package
+    // routes), one partner word joins the probe: the block that adds the most set bits.
     uint64_t s = 0x9E3779B97F4A7C15ull;
     auto next = [&s]() {
         s ^= s >> 12;
@@ -70,6 +72,10 @@ void orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
     };
     const int g0 = std::min(N, 6), samples = 512;
     std::vector<uint32_t> acc(size_t(2 * W));
+    std::vector<std::vector<uint32_t>> sums(size_t(samples), std::vector<uint32_t>(size_t(2 * W)));
+    ProbeChoice pc;
+    pc.extra.assign(size_t(G), -1);
+    double base_mean = 0, gain_mean = 0;
     for (int j = 0; j < G; j++) {
         uint32_t *base = rows.data() + size_t(j) * N * 2 * W;
         std::vector<long> dx(size_t(W), 0), dz(size_t(W), 0);
@@ -79,15 +85,38 @@ void orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
                 const int r = int(next() % uint64_t(N));
                 for (int w = 0; w < 2 * W; w++) acc[size_t(w)] ^= base[size_t(r) * 2 * W + w];
             }
+            sums[size_t(smp)] = acc;
             for (int w = 0; w < W; w++) {
                 dx[size_t(w)] += __builtin_popcount(acc[size_t(w)]);
                 dz[size_t(w)] += __builtin_popcount(acc[size_t(W + w)]);
             }
         }
         for (int w = 0; w < W; w++)
-            if (dz[size_t(w)] > dx[size_t(w)])
+            if (dz[size_t(w)] > dx[size_t(w)]) {
                 for (int r = 0; r < N; r++) std::swap(base[size_t(r) * 2 * W + w], base[size_t(r) * 2 * W + W + w]);
+                for (auto &v : sums) std::swap(v[size_t(w)], v[size_t(W + w)]);
+            }
+        if (W == 1) continue;  // the fast path is exact already
+        // mean fold weight with the probe words, and with each partner word added
+        double fold = 0;
+        std::vector<double> with(size_t(W), 0);
+        for (const auto &v : sums) {
+            uint32_t u = 0;
+            for (int w = 0; w < W; w++) u |= v[size_t(w)];
+            fold += __builtin_popcount(u);
+            for (int e = 0; e < W; e++) with[size_t(e)] += __builtin_popcount(u | v[size_t(W + e)]);
+        }
+        int best = 0;
+        for (int e = 1; e < W; e++)
+            if (with[size_t(e)] > with[size_t(best)]) best = e;
+        pc.extra[size_t(j)] = best;
+        base_mean += fold / samples / G;
+        gain_mean += (with[size_t(best)] - fold) / samples / G;
     }
+    // one more LOP3 per candidate pays only when the plain fold leaves the false-positive rate
+    // high: its mean sits well below the 32 bits a word can show
+    pc.use_extra = W > 1 && base_mean < 22.0 && gain_mean >= 2.0;
+    return pc;
 }
 
 int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, std::vector<uint64_t> &out) {
@@ -209,7 +238,16 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
             }
         }
     lap("rows");
-    if (!packaged_) orient_probe_words(h_rows_, G_, N_, W_);
+    const ProbeChoice probe = orient_probe_words(h_rows_, G_, N_, W_);
+    K_ = W_ == 1 ? 2 : W_ + (probe.use_extra ? 1 : 0);
+    h_prows_.assign(size_t(G_) * N_ * K_, 0);
+    for (int j = 0; j < G_; j++)
+        for (int r = 0; r < N_; r++) {
+            const uint32_t *src = h_rows_.data() + (size_t(j) * N_ + r) * 2 * W_;
+            uint32_t *dst = h_prows_.data() + (size_t(j) * N_ + r) * K_;
+            for (int w = 0; w < std::min(K_, W_ == 1 ? 2 : W_); w++) dst[w] = src[w];
+            if (K_ > W_ && W_ > 1) dst[W_] = src[W_ + probe.extra[size_t(j)]];
+        }
     lap("orient");
     SW_ = build_syndromes(gammas_, n, filter, h_syn_);
     lap("syndromes");
@@ -238,6 +276,49 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
                                              b = m ? ws[size_t(q + 1) * BK_ + m - 1] * pk[size_t(q)].size() : 0;
                     ws[size_t(q) * BK_ + m] = (a >= cap || b >= cap || a + b >= cap) ? cap : a + b;
                 }
+        }
+        // expanded elements (package members) in forward and reversed package order, and the
+        // weighted colex counts F / FR of the packaged tile kernel
+        for (int j = 0; j < G_; j++) {
+            int e = 0;
+            for (const auto &pk : gammas_[size_t(j)].packages) e += int(pk.size());
+            E_ = std::max(E_, e);
+        }
+        h_e_row_.assign(size_t(G_) * E_, -1);
+        h_e_pkg_.assign(size_t(G_) * E_, -1);
+        h_r_row_.assign(size_t(G_) * E_, -1);
+        h_r_pkg_.assign(size_t(G_) * E_, -1);
+        h_off_.assign(size_t(G_) * (P_ + 1), 0);
+        h_r_off_.assign(size_t(G_) * (P_ + 1), 0);
+        h_F_.assign(size_t(G_) * (E_ + 1) * BK_, 0);
+        h_FR_.assign(size_t(G_) * (E_ + 1) * BK_, 0);
+        for (int j = 0; j < G_; j++) {
+            const auto &pk = gammas_[size_t(j)].packages;
+            const int np = int(pk.size());
+            for (int dir = 0; dir < 2; dir++) {
+                short *erow = (dir ? h_r_row_ : h_e_row_).data() + size_t(j) * E_;
+                short *epkg = (dir ? h_r_pkg_ : h_e_pkg_).data() + size_t(j) * E_;
+                short *off = (dir ? h_r_off_ : h_off_).data() + size_t(j) * (P_ + 1);
+                unsigned long long *F = (dir ? h_FR_ : h_F_).data() + size_t(j) * (E_ + 1) * BK_;
+                int e = 0;
+                for (int qq = 0; qq < np; qq++) {
+                    const int q = dir ? np - 1 - qq : qq;  // reversed: package np-1-q' at position q'
+                    off[qq] = short(e);
+                    for (int r : pk[size_t(q)]) {
+                        erow[e] = short(r);
+                        epkg[e] = short(qq);
+                        e++;
+                    }
+                }
+                for (int qq = np; qq <= P_; qq++) off[qq] = short(e);
+                for (int x = 0; x <= e; x++) F[size_t(x) * BK_] = 1;
+                for (int x = 1; x <= e; x++)
+                    for (int i = 1; i < BK_; i++) {
+                        const unsigned long long a = F[size_t(x - 1) * BK_ + i],
+                                                 b = F[size_t(off[epkg[x - 1]]) * BK_ + i - 1];
+                        F[size_t(x) * BK_ + i] = (a >= cap || b >= cap || a + b >= cap) ? cap : a + b;
+                    }
+            }
         }
     }
     upload();
@@ -360,15 +441,19 @@ void Plan::upload() {
     stream_ = opts_.stream ? static_cast<cudaStream_t>(opts_.stream) : thread_stream(device_);
     // tile unit tables: level g needs G * (N - g + 1) + 1 entries (boundaries b in [h, N - t])
     table_cap_ = size_t(G_) * size_t(N_ + 1) * size_t(N_ + 2) / 2 + size_t(N_ + 2);
+    const size_t b_prows = align256(h_prows_.size() * 4);
     const size_t b_rows = align256(h_rows_.size() * 4), b_syn = align256(std::max<size_t>(h_syn_.size(), 1) * 8),
                  b_binom = align256(h_binom_.size() * 8),
                  b_state = align256(sizeof(LevelState) + size_t(max_weight_ + 1) * 8),
                  b_ctl = align256(sizeof(RunCtl)), b_trace = align256(size_t(N_ + 1) * 4),
                  b_counters = align256(size_t(N_ + 1) * 8), b_tables = align256(table_cap_ * 8);
     const size_t b_pkr = align256(h_pk_rows_.size() * 2 + 2), b_pks = align256(h_pk_size_.size() + 1),
-                 b_ws = align256(h_wsuf_.size() * 8 + 8);
-    d_bytes_ = b_rows + b_syn + b_binom + b_state + b_ctl + b_trace + 2 * b_counters + b_tables +
-               (packaged_ ? b_pkr + b_pks + b_ws : 0);
+                 b_ws = align256(h_wsuf_.size() * 8 + 8), b_el = align256(h_e_row_.size() * 2 + 2),
+                 b_off = align256(h_off_.size() * 2 + 2), b_F = align256(h_F_.size() * 8 + 8);
+    if (packaged_) table_cap_ += size_t(G_) * size_t(P_ + 1) * size_t(P_ + 2);  // room for the pair lists
+    const size_t b_tables_pk = align256(table_cap_ * 8);
+    d_bytes_ = b_prows + b_rows + b_syn + b_binom + b_state + b_ctl + b_trace + 2 * b_counters +
+               (packaged_ ? b_tables_pk + b_pkr + b_pks + b_ws + 4 * b_el + 2 * b_off + 2 * b_F : b_tables);
     const auto t0 = std::chrono::steady_clock::now();
     d_mem_ = workspace_get(device_, d_bytes_);
     unsigned char *base = static_cast<unsigned char *>(d_mem_);
@@ -397,7 +482,11 @@ void Plan::upload() {
     q += b_counters;
     d_tables_ = reinterpret_cast<unsigned long long *>(q);
     h_pinned_ = static_cast<unsigned long long *>(pinned_get(table_cap_ * 8));
-    q += b_tables;
+    q += packaged_ ? b_tables_pk : b_tables;
+    pd_.prows = reinterpret_cast<const uint32_t *>(q);
+    pd_.K = K_;
+    check_cuda(cudaMemcpyAsync(q, h_prows_.data(), h_prows_.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D probes");
+    q += b_prows;
     if (packaged_) {
         pk_.pk_rows = reinterpret_cast<const short *>(q);
         check_cuda(cudaMemcpyAsync(q, h_pk_rows_.data(), h_pk_rows_.size() * 2, cudaMemcpyHostToDevice, stream_),
@@ -410,6 +499,22 @@ void Plan::upload() {
         pk_.wsuf = reinterpret_cast<const unsigned long long *>(q);
         check_cuda(cudaMemcpyAsync(q, h_wsuf_.data(), h_wsuf_.size() * 8, cudaMemcpyHostToDevice, stream_),
                    "H2D packages");
+        q += b_ws;
+        auto put = [&](const void *src, size_t bytes, size_t region) {
+            check_cuda(cudaMemcpyAsync(q, src, bytes, cudaMemcpyHostToDevice, stream_), "H2D package tables");
+            unsigned char *at = q;
+            q += region;
+            return at;
+        };
+        pt_.e_row = reinterpret_cast<const short *>(put(h_e_row_.data(), h_e_row_.size() * 2, b_el));
+        pt_.e_pkg = reinterpret_cast<const short *>(put(h_e_pkg_.data(), h_e_pkg_.size() * 2, b_el));
+        pt_.r_row = reinterpret_cast<const short *>(put(h_r_row_.data(), h_r_row_.size() * 2, b_el));
+        pt_.r_pkg = reinterpret_cast<const short *>(put(h_r_pkg_.data(), h_r_pkg_.size() * 2, b_el));
+        pt_.off = reinterpret_cast<const short *>(put(h_off_.data(), h_off_.size() * 2, b_off));
+        pt_.r_off = reinterpret_cast<const short *>(put(h_r_off_.data(), h_r_off_.size() * 2, b_off));
+        pt_.F = reinterpret_cast<const unsigned long long *>(put(h_F_.data(), h_F_.size() * 8, b_F));
+        pt_.FR = reinterpret_cast<const unsigned long long *>(put(h_FR_.data(), h_FR_.size() * 8, b_F));
+        pt_.E = E_;
         pk_.P = P_;
         for (int j = 0; j < G_; j++) pk_.np[j] = np_[size_t(j)];
         upload_bytes += h_pk_rows_.size() * 2 + h_pk_size_.size() + h_wsuf_.size() * 8;
@@ -440,7 +545,7 @@ cudaEvent_t Plan::level_event(int i) {
     return events_[size_t(i)];
 }
 
-size_t tile_smem_bytes(int G, int N, int W, int SW, int BK);
+size_t tile_smem_bytes(int G, int N, int W, int K, int BK);
 
 TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
                        int world) {
@@ -509,6 +614,91 @@ long long Plan::lower_bound(int g) const {
     throw InvalidArgument("lower_bound: symplectic mode takes one or two matrices");
 }
 
+// Packaged levels: the head x tail tile kernel when the cost model prefers it to the walk
+// (same model as choose_tile, with the weighted element counts F / FR in place of binomials).
+bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
+    if (opts_.kernel == 1 || g < 2) return false;
+    const unsigned long long total = level_candidates(g);
+    if (opts_.kernel != 2 && total < (1ull << 16)) return false;
+    const double Hl = heads_per_lane(W_), HBk = head_block(W_);
+    const double slots = double(num_sms_) * tile_blocks_per_sm(W_) * std::max(1, world);
+    double best_time = opts_.kernel == 2 ? 1e300 : double(total) * 28.0 / slots;
+    int best_t = 0, best_chunk = kTailChunk;
+    auto Hb_of = [&](int j, int b, int h) { return double(F_at(j, h_off_[size_t(j) * (P_ + 1) + b], h)); };
+    auto Tb_of = [&](int j, int b, int t) {
+        const int np = np_[size_t(j)];
+        const short *off = h_off_.data() + size_t(j) * (P_ + 1);
+        return double(off[b + 1] - off[b]) * double(FR_at(j, h_r_off_[size_t(j) * (P_ + 1) + (np - 1 - b)], t - 1));
+    };
+    for (int t = 1; t < g; t++) {
+        const int h = g - t;
+        for (int tchunk = kTailChunk; tchunk >= 64; tchunk /= 2) {
+            double sum = 0, biggest = 0;
+            for (int j = 0; j < G_; j++)
+                for (int b = h; b <= np_[size_t(j)] - t; b++) {
+                    const double Hb = Hb_of(j, b, h), Tb = Tb_of(j, b, t);
+                    if (Hb <= 0 || Tb <= 0) continue;
+                    const double nH = std::ceil(Hb / HBk), nT = std::ceil(Tb / tchunk);
+                    const double heads_last = Hb - (nH - 1) * HBk;
+                    const double warps_full = kTileThreads / 32.0, warps_last = std::ceil(heads_last / (32.0 * Hl));
+                    const double tc = Tb / nT;
+                    const double unit_full = warps_full * 32 * Hl * tc + 25000, unit_last = warps_last * 32 * Hl * tc + 25000;
+                    sum += nT * ((nH - 1) * unit_full + unit_last);
+                    biggest = std::max(biggest, nH > 1 ? unit_full : unit_last);
+                }
+            const double time = std::max(sum / slots, biggest);
+            if (time < best_time) {
+                best_time = time;
+                best_t = t;
+                best_chunk = tchunk;
+            }
+        }
+    }
+    if (best_t == 0) return false;
+    if (ptile_smem_bytes(G_, N_, W_, K_, P_, E_, std::min(BK_, g + 2)) > 200 * 1024) return false;
+    PTilePlan &tp = lv.ptile;
+    tp.g = g;
+    tp.t = best_t;
+    tp.h = g - best_t;
+    tp.tchunk = best_chunk;
+    tp.thr0 = ~0u;
+    // (Gamma, b) pairs with work, their cumulative unit counts, then the pair codes
+    std::vector<unsigned long long> cum;
+    std::vector<unsigned> pairs;
+    unsigned long long acc = 0;
+    for (int j = 0; j < G_; j++)
+        for (int b = tp.h; b <= np_[size_t(j)] - tp.t; b++) {
+            const unsigned long long Hb = F_at(j, h_off_[size_t(j) * (P_ + 1) + b], tp.h);
+            const int np = np_[size_t(j)];
+            const short *off = h_off_.data() + size_t(j) * (P_ + 1);
+            const unsigned long long Tb =
+                (unsigned long long)(off[b + 1] - off[b]) * FR_at(j, h_r_off_[size_t(j) * (P_ + 1) + (np - 1 - b)], tp.t - 1);
+            if (Hb == 0 || Tb == 0) continue;
+            cum.push_back(acc);
+            pairs.push_back(unsigned(j) << 16 | unsigned(b));
+            acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
+        }
+    cum.push_back(acc);
+    tp.npairs = int(pairs.size());
+    const size_t n_entries = cum.size() + (pairs.size() + 1) / 2;
+    if (table_used_ + n_entries > table_cap_) return false;
+    unsigned long long *h_table = h_pinned_ + table_used_;
+    std::copy(cum.begin(), cum.end(), h_table);
+    std::memcpy(h_table + cum.size(), pairs.data(), pairs.size() * 4);
+    tp.cum = d_tables_ + table_used_;
+    tp.pairs = reinterpret_cast<const unsigned *>(d_tables_ + table_used_ + cum.size());
+    tp.counter = d_counters_ + g;
+    tp.unit_total = acc;
+    tp.shard_rank = rank;
+    tp.shard_world = world;
+    table_used_ += n_entries;
+    check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table, n_entries * 8, cudaMemcpyHostToDevice,
+                               stream_),
+               "H2D unit table");
+    lv.t = -2;
+    return true;
+}
+
 unsigned long long Plan::level_candidates(int g) const {
     if (!packaged_) return binom_u64(N_, g) * (unsigned long long)G_;
     unsigned long long t = 0;
@@ -527,6 +717,10 @@ void Plan::prepare_level(int g) {
     const int world = lv.sharded ? std::max(1, opts_.world) : 1, rank = lv.sharded ? opts_.rank : 0;
     if (packaged_) {
         if (g >= BK_) throw InvalidArgument("generation beyond the kernels' combination-size limit");
+        if (prepare_ptile(g, lv, world, rank)) {
+            lv.ready = true;
+            return;
+        }
         PkgLevel &L = lv.pkg;
         L.g = g;
         L.thr0 = ~0u;
@@ -599,7 +793,7 @@ void Plan::prepare_level(int g) {
         check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tp.cum), h_table, n_entries * 8,
                                    cudaMemcpyHostToDevice, stream_),
                    "H2D unit table");
-        if (tile_smem_bytes(G_, N_, W_, SW_, std::min(BK_, g + 2)) > 200 * 1024)
+        if (tile_smem_bytes(G_, N_, W_, K_, std::min(BK_, g + 2)) > 200 * 1024)
             throw InvalidArgument("problem too large for shared-memory staging");
     }
     lv.ready = true;
@@ -633,9 +827,10 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         prepare_level(g);
         const LevelHost &lv = levels_[size_t(g)];
         check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
-        const int nl = lv.t < 0    ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
-                       : lv.t == 0 ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
-                                   : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
+        const int nl = lv.t == -2  ? launch_ptile_level(pd_, pk_, pt_, lv.ptile, stream_, num_sms_)
+                       : lv.t == -1 ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
+                       : lv.t == 0  ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
+                                    : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
         if (nl < 0) throw InvalidArgument("unsupported row width");
         launches += nl;
         check_cuda(cudaGetLastError(), "level kernel launch");

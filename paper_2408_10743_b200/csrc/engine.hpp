@@ -66,11 +66,13 @@ class Plan {
         LevelLaunch walk{};
         TilePlan tile{};
         PkgLevel pkg{};
+        PTilePlan ptile{};
     };
 
     void upload();
     long long lower_bound(int g) const;
     void prepare_level(int g);
+    bool prepare_ptile(int g, LevelHost &lv, int world, int rank);
     cudaEvent_t level_event(int i);
 
     std::vector<GammaIn> gammas_;
@@ -80,6 +82,8 @@ class Plan {
     int G_ = 0, N_ = 0, W_ = 0, SW_ = 0, BK_ = 0, scale_ = 1, max_weight_ = 0, sentinel_ = 0;
     bool image_layout_ = false;
     std::vector<uint32_t> h_rows_;
+    std::vector<uint32_t> h_prows_;  // [G][N][K_] the tile kernels' probe words
+    int K_ = 1;
     std::vector<uint64_t> h_syn_;
     std::vector<unsigned long long> h_binom_;
     int device_ = 0, num_sms_ = 148;
@@ -103,6 +107,13 @@ class Plan {
     std::vector<unsigned char> h_pk_size_;       // [G][P]
     std::vector<unsigned long long> h_wsuf_;     // [G][P + 1][BK]
     PkgDev pk_{};
+    // packaged tile kernel: expanded elements and weighted colex counts (PtileDev)
+    int E_ = 0;
+    std::vector<short> h_e_row_, h_e_pkg_, h_r_row_, h_r_pkg_, h_off_, h_r_off_;
+    std::vector<unsigned long long> h_F_, h_FR_;
+    PtileDev pt_{};
+    unsigned long long F_at(int j, int x, int i) const { return h_F_[(size_t(j) * (E_ + 1) + x) * BK_ + i]; }
+    unsigned long long FR_at(int j, int x, int i) const { return h_FR_[(size_t(j) * (E_ + 1) + x) * BK_ + i]; }
     unsigned long long level_candidates(int g) const;
     void unrank_best(int g, int j, unsigned long long r, std::vector<uint64_t> &acc) const;
 };
@@ -122,7 +133,11 @@ int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int 
 // Per Gamma and 32-symbol block, swap the x- and z-words of every row so that the word the
 // tile kernel's fast path folds (the first of the block) is the denser one. Weights are
 // unchanged (popc(x|z) is symmetric).
-void orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W);
+struct ProbeChoice {
+    std::vector<int> extra;  // per Gamma: the block whose partner word may join the probe
+    bool use_extra = false;  // probe words per row = W + 1 (else W; 2 when W = 1)
+};
+ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W);
 
 // Saturating binomial table (N+1) x BK.
 std::vector<unsigned long long> binom_table(int N, int BK);

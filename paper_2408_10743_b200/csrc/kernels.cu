@@ -524,21 +524,21 @@ __device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan t
     return wv;
 }
 
-// Fast-path lower bound on a candidate's weight (in symbols), one POPC whatever W is:
-// the OR over the W blocks of the probe-word differences. Bit b of the fold is set only if
-// some symbol 32w+b of the candidate is nonzero, so popc(fold) <= popc(x|z). W = 1 folds
-// both words of its single block and is exact.
-template <int W>
-__device__ __forceinline__ uint32_t probe_fold(const uint32_t (&hp)[W], const uint32_t (&hq)[W], const uint32_t *t) {
-    if constexpr (W == 1) {
-        return (hp[0] ^ t[0]) | (hq[0] ^ t[1]);
-    } else {
-        uint32_t u = hp[0] ^ t[0];
+// Fast-path lower bound on a candidate's weight (in symbols), one POPC whatever W is: the OR
+// of the probe-word differences. The probe words of a row (ProblemDev.prows, K per row) are
+// the oriented word of each 32-symbol block, plus — for Gammas whose probe words alone are
+// sparse — the partner word of one block; W = 1 keeps both words of its block. Bit b of the
+// fold is set only if a symbol 32w+b of the candidate is nonzero, so popc(fold) <= popc(x|z)
+// (exact for W = 1).
+template <int K>
+__device__ __forceinline__ uint32_t probe_fold(const uint32_t (&hp)[K], const uint32_t *t) {
+    uint32_t u = hp[0] ^ t[0];
 #pragma unroll
-        for (int w = 1; w < W; w++) u |= hp[w] ^ t[w];
-        return u;
-    }
+    for (int w = 1; w < K; w++) u |= hp[w] ^ t[w];
+    return u;
 }
+
+SDB_HD constexpr int probe_words(int W, bool XP) { return W == 1 ? 2 : W + (XP ? 1 : 0); }
 
 // colex successor of the ascending m-subset e (m >= 1) with the row sum kept in acc:
 // the lowest element that can move up by one moves, the ones below it reset to 0..q-1.
@@ -558,12 +558,12 @@ __device__ __forceinline__ void colex_step(int *e, int m, uint32_t (&acc)[NW], c
         for (int w = 0; w < NW; w++) acc[w] ^= base[(off + e[k]) * rowlen + w];
 }
 
-template <int W>
+template <int W, bool XP>
 __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kernel(ProblemDev p, TilePlan tp) {
     constexpr int H = heads_per_lane(W);
     constexpr int HB = head_block(W);
-    constexpr int PW = probe_stride(W);
-    constexpr int NW = W == 1 ? 2 : W;  // words of each row the fast path reads
+    constexpr int K = probe_words(W, XP);  // probe words per row / head / tail
+    constexpr int PW = probe_stride(K);
     if (run_done(p)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowlen = 2 * W;
@@ -571,15 +571,17 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
     // binomials C(a, k) for k <= g + 1 only: the level needs no wider ones, and the slice keeps
     // shared memory small enough for many resident CTAs
     const int BKs = min(p.BK, tp.g + 2);
-    const TileSmem lay = tile_smem_layout(G, N, W, BKs);
+    const TileSmem lay = tile_smem_layout(G, N, W, K, BKs);
     const int nrow_words = G * N * rowlen;
     uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem + lay.rows);
     unsigned long long *s_binom = reinterpret_cast<unsigned long long *>(smem + lay.binom);
     const int nbinom = (N + 1) * BKs;
     uint32_t *s_tp = reinterpret_cast<uint32_t *>(smem + lay.tp);
+    uint32_t *s_prows = reinterpret_cast<uint32_t *>(smem + lay.prows);
     __shared__ TileUnit s_un;
     __shared__ unsigned long long s_visited;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
+    for (int i = threadIdx.x; i < G * N * K; i += blockDim.x) s_prows[i] = p.prows[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
     if (threadIdx.x == 0) s_visited = 0;
 
@@ -619,7 +621,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
         const int t = tp.t, h = tp.h;
         {
             const int b = s_un.b;
-            const uint32_t *grows = s_rows + s_un.j * N * rowlen;
+            const uint32_t *pg = s_prows + s_un.j * N * K;  // probe words of this Gamma's rows
             // stage the tail chunk's probe words: {b} + colex (t-1)-subsets of (b, N);
             // each thread takes a contiguous run and walks it with colex successors
             const int R = (tcount + blockDim.x - 1) / blockDim.x;
@@ -627,20 +629,20 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
             if (i0 < i1) {
                 int e[kMaxLevel];
                 unrank_colex(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, BKs, e);
-                uint32_t acc[NW];
+                uint32_t acc[K];
 #pragma unroll
-                for (int w = 0; w < NW; w++) acc[w] = grows[b * rowlen + w];
+                for (int w = 0; w < K; w++) acc[w] = pg[b * K + w];
                 for (int k = 0; k < t - 1; k++)
 #pragma unroll
-                    for (int w = 0; w < NW; w++) acc[w] ^= grows[(b + 1 + e[k]) * rowlen + w];
+                    for (int w = 0; w < K; w++) acc[w] ^= pg[(b + 1 + e[k]) * K + w];
                 for (int i = i0;;) {
 #pragma unroll
-                    for (int w = 0; w < NW; w++) s_tp[i * PW + w] = acc[w];
+                    for (int w = 0; w < K; w++) s_tp[i * PW + w] = acc[w];
                     if (i == tcount - 1 && (tcount & 1))  // odd counts: duplicate the last tail
 #pragma unroll
-                        for (int w = 0; w < NW; w++) s_tp[(i + 1) * PW + w] = acc[w];
+                        for (int w = 0; w < K; w++) s_tp[(i + 1) * PW + w] = acc[w];
                     if (++i >= i1) break;
-                    colex_step<NW>(e, t - 1, acc, grows, b + 1, rowlen);
+                    colex_step<K>(e, t - 1, acc, pg, b + 1, K);
                 }
             }
         }
@@ -649,31 +651,30 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
         // this lane's heads: H consecutive colex ranks of h-subsets of [0, b)
         const int nvalid = max(0, min(H, s_un.pad - lane_head));
         if (!__any_sync(0xffffffffu, nvalid > 0)) continue;
-        uint32_t hp[H][W], hq[W == 1 ? H : 1][W];
+        uint32_t hp[H][K];
         {
             const int b = s_un.b;
-            const uint32_t *grows = s_rows + s_un.j * N * rowlen;
+            const uint32_t *pg = s_prows + s_un.j * N * K;
             int e[kMaxLevel];
-            uint32_t acc[NW];
+            uint32_t acc[K];
             if (nvalid > 0) {
                 unrank_colex(s_un.hbase0 + lane_head, h, b, s_binom, BKs, e);
 #pragma unroll
-                for (int w = 0; w < NW; w++) acc[w] = 0;
+                for (int w = 0; w < K; w++) acc[w] = 0;
                 for (int k = 0; k < h; k++)
 #pragma unroll
-                    for (int w = 0; w < NW; w++) acc[w] ^= grows[e[k] * rowlen + w];
+                    for (int w = 0; w < K; w++) acc[w] ^= pg[e[k] * K + w];
             } else {
                 // lanes without heads: all-ones probe words, the fold never passes the check
 #pragma unroll
-                for (int w = 0; w < NW; w++) acc[w] = 0xffffffffu;
+                for (int w = 0; w < K; w++) acc[w] = 0xffffffffu;
             }
 #pragma unroll
             for (int i = 0; i < H; i++) {
-                if (i > 0 && i < nvalid) colex_step<NW>(e, h, acc, grows, 0, rowlen);
+                if (i > 0 && i < nvalid) colex_step<K>(e, h, acc, pg, 0, K);
                 // heads past the valid count repeat the last valid head (same candidates)
 #pragma unroll
-                for (int w = 0; w < W; w++) hp[i][w] = acc[w];
-                if constexpr (W == 1) hq[i][0] = acc[1];
+                for (int w = 0; w < K; w++) hp[i][w] = acc[w];
             }
         }
 
@@ -695,8 +696,8 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
                 unsigned m = 0xffffffffu;
 #pragma unroll
                 for (int i = 0; i < H; i++) {
-                    const unsigned a = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt));
-                    const unsigned c = __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], tt + PW));
+                    const unsigned a = __popc(probe_fold<K>(hp[i], tt));
+                    const unsigned c = __popc(probe_fold<K>(hp[i], tt + PW));
                     m = min(m, min(a, c));
                 }
                 // warp-uniform exit: a lone lane leaving the loop would finish it alone later
@@ -710,7 +711,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
 #pragma unroll
                 for (int r = 0; r < 2; r++)
                     if (i < nvalid && ti + r < tcount &&
-                        __popc(probe_fold<W>(hp[i], hq[W == 1 ? i : 0], s_tp + (ti + r) * PW)) <= thr0)
+                        __popc(probe_fold<K>(hp[i], s_tp + (ti + r) * PW)) <= thr0)
                         fire |= 1u << (2 * i + r);
             }
             while (fire) {
@@ -726,24 +727,370 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kern
     if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
 }
 
-size_t tile_smem(int G, int N, int W, int SW, int BK) { (void)SW; return tile_smem_layout(G, N, W, BK).total; }
+// ---------------------------------------------------------------- packaged tile (1/3-packages)
 
+struct PtileSmem {
+    size_t rows, prows, el, off, F, FR, tp, total;
+};
+__host__ __device__ inline PtileSmem ptile_layout(int G, int N, int W, int K, int P, int E, int BKs) {
+    PtileSmem L{};
+    L.rows = 0;
+    L.prows = align16(size_t(G) * N * 2 * W * 4);
+    L.el = align16(L.prows + size_t(G) * N * K * 4);                 // e_row, e_pkg, r_row, r_pkg
+    L.off = align16(L.el + size_t(4) * G * E * 2);                   // off, r_off
+    L.F = align16(L.off + size_t(2) * G * (P + 1) * 2);              // F sliced to BKs columns
+    L.FR = align16(L.F + size_t(G) * (E + 1) * BKs * 8);
+    L.tp = align16(L.FR + size_t(G) * (E + 1) * BKs * 8);
+    L.total = align16(L.tp + size_t(kTailChunk + 1) * probe_stride(K) * 4);
+    return L;
+}
+
+// colex unrank of rho into m elements with distinct packages inside elements [0, lim):
+// the largest x with F(x, i) <= rho is the i-th element; the rest lie below its package
+__device__ __forceinline__ void unrank_pcolex(unsigned long long rho, int m, int lim, const unsigned long long *F,
+                                              int BKs, const short *epkg, const short *off, int *e) {
+    int x = lim - 1;
+    for (int i = m; i >= 1; i--) {
+        while (F[x * BKs + i] > rho) x--;
+        e[i - 1] = x;
+        rho -= F[x * BKs + i];
+        x = off[epkg[x]] - 1;
+    }
+}
+
+// colex successor of the element set e[0..m) (distinct packages, all below lim) with the
+// row sum kept in acc: the lowest element that can move to the next element (next member,
+// or the first member of the next package, as long as it stays below the package of the
+// element above it); the ones below restart at the first members of packages 0, 1, ...
+template <int NW>
+__device__ __forceinline__ void pcolex_step(int *e, int m, int lim, const short *epkg, const short *off,
+                                            const short *erow, uint32_t (&acc)[NW], const uint32_t *rows,
+                                            int rowlen) {
+    int i = 0;
+    for (;; i++) {
+        const int v = e[i] + 1;
+        if (i + 1 < m ? (v < e[i + 1] && epkg[v] != epkg[e[i + 1]]) : v < lim) break;
+    }
+    for (int k = 0; k <= i; k++)
+#pragma unroll
+        for (int w = 0; w < NW; w++) acc[w] ^= rows[erow[e[k]] * rowlen + w];
+    e[i]++;
+    for (int k = 0; k < i; k++) e[k] = off[k];
+    for (int k = 0; k <= i; k++)
+#pragma unroll
+        for (int w = 0; w < NW; w++) acc[w] ^= rows[erow[e[k]] * rowlen + w];
+}
+
+struct PtileUnit {
+    int j, b, tcount, heads;
+    int np, lim_h, lim_t, sb;             // packages, head / tail element limits, members of b
+    unsigned long long t0, hbase0, tsub;  // first tail, first head, tail sets per member of b
+};
+
+// Per-Gamma views of the packaged tables in shared memory.
+struct PtileView {
+    const short *erow, *epkg, *rrow, *rpkg, *off, *roff;
+    const unsigned long long *F, *FR;
+};
+__device__ __forceinline__ PtileView ptile_view(const short *s_el, const short *s_off, const unsigned long long *s_F,
+                                                const unsigned long long *s_FR, int G, int E, int P, int BKs, int j) {
+    PtileView v;
+    v.erow = s_el + j * E;
+    v.epkg = s_el + G * E + j * E;
+    v.rrow = s_el + 2 * G * E + j * E;
+    v.rpkg = s_el + 3 * G * E + j * E;
+    v.off = s_off + j * (P + 1);
+    v.roff = s_off + G * (P + 1) + j * (P + 1);
+    v.F = s_F + size_t(j) * (E + 1) * BKs;
+    v.FR = s_FR + size_t(j) * (E + 1) * BKs;
+    return v;
+}
+
+// Rare path: rebuild the candidate's (package, member) list from the ranks, exact weight,
+// admissibility, key = the reference's lexicographic rank over (p_1, m_1, p_2, m_2, ...)
+// (engine.cpp:202-219) through the weighted suffix counts.
 template <int W>
-int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, int num_sms) {
-    const size_t smem = tile_smem(p.G, p.N, W, p.SW, min(p.BK, tp.g + 2));
+__device__ __noinline__ unsigned ptile_exact(const ProblemDev p, const PkgDev k, const PTilePlan tp,
+                                             const uint32_t *s_rows, const PtileView v, int BKs, const PtileUnit *un,
+                                             int head_off, int tix, unsigned thrH) {
+    const int N = p.N, h = tp.h, t = tp.t, g = tp.g, j = un->j, b = un->b, np = un->np;
+    int e[kMaxLevel], pk[kMaxLevel], mm[kMaxLevel], row[kMaxLevel];
+    unrank_pcolex(un->hbase0 + head_off, h, un->lim_h, v.F, BKs, v.epkg, v.off, e);
+    for (int i = 0; i < h; i++) {
+        pk[i] = v.epkg[e[i]];
+        mm[i] = e[i] - v.off[pk[i]];
+        row[i] = v.erow[e[i]];
+    }
+    const unsigned long long tau = un->t0 + tix;
+    const int mb = int(tau / un->tsub);
+    pk[h] = b;
+    mm[h] = mb;
+    row[h] = v.erow[v.off[b] + mb];
+    unrank_pcolex(tau % un->tsub, t - 1, un->lim_t, v.FR, BKs, v.rpkg, v.roff, e);
+    for (int i = 0; i < t - 1; i++) {  // reversed order: the last reversed element is the next package
+        const int er = e[t - 2 - i], rq = v.rpkg[er];
+        pk[h + 1 + i] = np - 1 - rq;
+        mm[h + 1 + i] = er - v.roff[rq];
+        row[h + 1 + i] = v.rrow[er];
+    }
+    uint32_t acc[2 * W];
+#pragma unroll
+    for (int w = 0; w < 2 * W; w++) acc[w] = 0;
+    const uint32_t *grows = s_rows + j * N * 2 * W;
+    for (int i = 0; i < g; i++) xor_row<W>(acc, grows + row[i] * 2 * W);
+    const unsigned wv = unsigned(p.scale * weight_of<W>(acc));
+    if (wv > thrH) return thrH;
+    if (p.SW) {
+        const unsigned long long *syn = p.syn + (size_t)j * N * p.SW;
+        bool adm = false;
+        for (int s = 0; s < p.SW; s++) {
+            unsigned long long x = 0;
+            for (int i = 0; i < g; i++) x ^= syn[row[i] * p.SW + s];
+            adm |= x != 0;
+        }
+        if (!adm) return thrH;
+    }
+    const unsigned long long *ws = k.wsuf + size_t(j) * (k.P + 1) * p.BK;
+    const unsigned char *psz = k.pk_size + j * k.P;
+    unsigned long long rank = 0;
+    int prev = -1;
+    for (int i = 0; i < g; i++) {
+        for (int q = prev + 1; q < pk[i]; q++) rank += psz[q] * ws[(q + 1) * p.BK + (g - 1 - i)];
+        rank += (unsigned long long)mm[i] * ws[(pk[i] + 1) * p.BK + (g - 1 - i)];
+        prev = pk[i];
+    }
+    const unsigned long long key = ((unsigned long long)j << kKeyRankBits) | rank;
+    atomicMin(&p.state->wmin, wv);
+    atomicMin(&p.key_by_w[wv], key);
+    return wv;
+}
+
+template <int W, bool XP>
+__global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W))
+    ptile_kernel(ProblemDev p, PkgDev k, PtileDev d, PTilePlan tp) {
+    constexpr int H = heads_per_lane(W);
+    constexpr int HB = head_block(W);
+    constexpr int K = probe_words(W, XP);
+    constexpr int PW = probe_stride(K);
+    if (run_done(p)) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int rowlen = 2 * W, G = p.G, N = p.N, P = k.P, E = d.E;
+    const int BKs = min(p.BK, tp.g + 2);
+    const PtileSmem lay = ptile_layout(G, N, W, K, P, E, BKs);
+    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem + lay.rows);
+    short *s_el = reinterpret_cast<short *>(smem + lay.el);
+    short *s_off = reinterpret_cast<short *>(smem + lay.off);
+    unsigned long long *s_F = reinterpret_cast<unsigned long long *>(smem + lay.F);
+    unsigned long long *s_FR = reinterpret_cast<unsigned long long *>(smem + lay.FR);
+    uint32_t *s_tp = reinterpret_cast<uint32_t *>(smem + lay.tp);
+    uint32_t *s_prows = reinterpret_cast<uint32_t *>(smem + lay.prows);
+    __shared__ PtileUnit s_un;
+    __shared__ unsigned long long s_visited;
+    for (int i = threadIdx.x; i < G * N * rowlen; i += blockDim.x) s_rows[i] = p.rows[i];
+    for (int i = threadIdx.x; i < G * N * K; i += blockDim.x) s_prows[i] = p.prows[i];
+    for (int i = threadIdx.x; i < G * E; i += blockDim.x) {
+        s_el[i] = d.e_row[i];
+        s_el[G * E + i] = d.e_pkg[i];
+        s_el[2 * G * E + i] = d.r_row[i];
+        s_el[3 * G * E + i] = d.r_pkg[i];
+    }
+    for (int i = threadIdx.x; i < G * (P + 1); i += blockDim.x) {
+        s_off[i] = d.off[i];
+        s_off[G * (P + 1) + i] = d.r_off[i];
+    }
+    for (int i = threadIdx.x; i < G * (E + 1) * BKs; i += blockDim.x) {
+        const int x = i / BKs, c = i % BKs;
+        s_F[i] = d.F[size_t(x) * p.BK + c];
+        s_FR[i] = d.FR[size_t(x) * p.BK + c];
+    }
+    if (threadIdx.x == 0) s_visited = 0;
+
+    const unsigned sshift = p.scale == 2 ? 1u : 0u;
+    const int lane_head = (threadIdx.x >> 5) * (32 * H) + (threadIdx.x & 31) * H;
+    unsigned thrH = start_threshold(p, tp.thr0);
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long unit = atomicAdd(tp.counter, 1ull) * tp.shard_world + tp.shard_rank;
+            s_un.tcount = 0;
+            if (unit < tp.unit_total) {
+                int lo = 0, hi = tp.npairs - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (__ldg(tp.cum + mid) <= unit) lo = mid; else hi = mid - 1;
+                }
+                const unsigned pr = __ldg(tp.pairs + lo);
+                const int j = int(pr >> 16), b = int(pr & 0xffffu);
+                const PtileView v = ptile_view(s_el, s_off, s_F, s_FR, G, E, P, BKs, j);
+                const int np = k.np[j];
+                const unsigned long long u = unit - __ldg(tp.cum + lo);
+                s_un.j = j;
+                s_un.b = b;
+                s_un.np = np;
+                s_un.lim_h = v.off[b];
+                s_un.lim_t = v.roff[np - 1 - b];
+                s_un.sb = v.off[b + 1] - v.off[b];
+                const unsigned long long Hb = v.F[s_un.lim_h * BKs + tp.h];
+                s_un.tsub = v.FR[s_un.lim_t * BKs + (tp.t - 1)];
+                const unsigned long long Tb = (unsigned long long)s_un.sb * s_un.tsub;
+                const unsigned long long nT = (Tb + tp.tchunk - 1) / tp.tchunk;
+                const unsigned long long hc = u / nT, tc = u % nT;
+                s_un.t0 = tc * tp.tchunk;
+                s_un.tcount = int(min((unsigned long long)tp.tchunk, Tb - s_un.t0));
+                s_un.hbase0 = hc * HB;
+                s_un.heads = int(min((unsigned long long)HB, Hb - hc * HB));
+                s_visited += (unsigned long long)s_un.heads * (unsigned long long)s_un.tcount;
+            }
+        }
+        __syncthreads();
+        const int tcount = s_un.tcount;
+        if (tcount == 0) break;
+        const int t = tp.t, h = tp.h, j = s_un.j;
+        const PtileView v = ptile_view(s_el, s_off, s_F, s_FR, G, E, P, BKs, j);
+        const uint32_t *pg = s_prows + j * N * K;  // probe words of this Gamma's rows
+        {
+            // stage tails: member mb of package b plus a (t-1)-set above b (reversed colex)
+            const int R = (tcount + blockDim.x - 1) / blockDim.x;
+            const int i0 = threadIdx.x * R, i1 = min(i0 + R, tcount);
+            if (i0 < i1) {
+                int e[kMaxLevel];
+                unsigned long long tau = s_un.t0 + i0;
+                int mb = int(tau / s_un.tsub);
+                unsigned long long rest = tau % s_un.tsub;
+                uint32_t acc[K];
+                auto restart = [&]() {
+                    unrank_pcolex(rest, t - 1, s_un.lim_t, v.FR, BKs, v.rpkg, v.roff, e);
+#pragma unroll
+                    for (int w = 0; w < K; w++) acc[w] = pg[v.erow[v.off[s_un.b] + mb] * K + w];
+                    for (int q = 0; q < t - 1; q++)
+#pragma unroll
+                        for (int w = 0; w < K; w++) acc[w] ^= pg[v.rrow[e[q]] * K + w];
+                };
+                restart();
+                for (int i = i0;;) {
+#pragma unroll
+                    for (int w = 0; w < K; w++) s_tp[i * PW + w] = acc[w];
+                    if (i == tcount - 1 && (tcount & 1))
+#pragma unroll
+                        for (int w = 0; w < K; w++) s_tp[(i + 1) * PW + w] = acc[w];
+                    if (++i >= i1) break;
+                    if (++rest == s_un.tsub) {  // next member of package b
+                        rest = 0;
+                        mb++;
+                        restart();
+                    } else {
+                        pcolex_step<K>(e, t - 1, s_un.lim_t, v.rpkg, v.roff, v.rrow, acc, pg, K);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        const int nvalid = max(0, min(H, s_un.heads - lane_head));
+        if (!__any_sync(0xffffffffu, nvalid > 0)) continue;
+        uint32_t hp[H][K];
+        {
+            int e[kMaxLevel];
+            uint32_t acc[K];
+#pragma unroll
+            for (int w = 0; w < K; w++) acc[w] = nvalid > 0 ? 0u : 0xffffffffu;
+            if (nvalid > 0) {
+                unrank_pcolex(s_un.hbase0 + lane_head, h, s_un.lim_h, v.F, BKs, v.epkg, v.off, e);
+                for (int q = 0; q < h; q++)
+#pragma unroll
+                    for (int w = 0; w < K; w++) acc[w] ^= pg[v.erow[e[q]] * K + w];
+            }
+#pragma unroll
+            for (int i = 0; i < H; i++) {
+                if (i > 0 && i < nvalid) pcolex_step<K>(e, h, s_un.lim_h, v.epkg, v.off, v.erow, acc, pg, K);
+#pragma unroll
+                for (int w = 0; w < K; w++) hp[i][w] = acc[w];
+            }
+        }
+
+        unsigned thr0 = thrH >> sshift;
+        int ti = 0;
+        for (;;) {
+            for (; ti < tcount; ti += 2) {
+                uint32_t tt[2 * PW];
+#pragma unroll
+                for (int vv = 0; vv < 2 * PW; vv += 4) {
+                    const uint4 q4 = *reinterpret_cast<const uint4 *>(s_tp + ti * PW + vv);
+                    tt[vv] = q4.x;
+                    tt[vv + 1] = q4.y;
+                    tt[vv + 2] = q4.z;
+                    tt[vv + 3] = q4.w;
+                }
+                unsigned m = 0xffffffffu;
+#pragma unroll
+                for (int i = 0; i < H; i++) {
+                    const unsigned a = __popc(probe_fold<K>(hp[i], tt));
+                    const unsigned c = __popc(probe_fold<K>(hp[i], tt + PW));
+                    m = min(m, min(a, c));
+                }
+                if (__any_sync(0xffffffffu, m <= thr0 && nvalid > 0)) break;
+            }
+            if (ti >= tcount) break;
+            unsigned fire = 0;
+#pragma unroll
+            for (int i = 0; i < H; i++) {
+#pragma unroll
+                for (int r = 0; r < 2; r++)
+                    if (i < nvalid && ti + r < tcount &&
+                        __popc(probe_fold<K>(hp[i], s_tp + (ti + r) * PW)) <= thr0)
+                        fire |= 1u << (2 * i + r);
+            }
+            while (fire) {
+                const int kk = __ffs(fire) - 1;
+                fire &= fire - 1;
+                thrH = ptile_exact<W>(p, k, tp, s_rows, v, BKs, &s_un, lane_head + (kk >> 1), ti + (kk & 1), thrH);
+            }
+            thr0 = thrH >> sshift;
+            ti += 2;
+        }
+        thrH = min(thrH, *(volatile unsigned int *)&p.state->wmin);
+    }
+    if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
+}
+
+template <int W, bool XP>
+int launch_ptile_impl(const ProblemDev &p, const PkgDev &k, const PtileDev &d, const PTilePlan &tp, cudaStream_t st,
+                      int num_sms) {
+    const size_t smem = ptile_layout(p.G, p.N, W, probe_words(W, XP), k.P, d.E, min(p.BK, tp.g + 2)).total;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(ptile_kernel<W, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<W>, kTileThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ptile_kernel<W, XP>, kTileThreads, smem);
     if (per_sm < 1) per_sm = 1;
     const unsigned long long units = (tp.unit_total + tp.shard_world - 1 - tp.shard_rank) / tp.shard_world;
     unsigned long long blocks = (unsigned long long)num_sms * per_sm;
     if (blocks > units) blocks = units;
     if (blocks == 0) return 0;
-    tile_kernel<W><<<unsigned(blocks), kTileThreads, smem, st>>>(p, tp);
+    ptile_kernel<W, XP><<<unsigned(blocks), kTileThreads, smem, st>>>(p, k, d, tp);
+    return 1;
+}
+
+size_t tile_smem(int G, int N, int W, int K, int BK) { return tile_smem_layout(G, N, W, K, BK).total; }
+
+template <int W, bool XP>
+int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, int num_sms) {
+    const size_t smem = tile_smem(p.G, p.N, W, probe_words(W, XP), min(p.BK, tp.g + 2));
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(tile_kernel<W, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<W, XP>, kTileThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const unsigned long long units = (tp.unit_total + tp.shard_world - 1 - tp.shard_rank) / tp.shard_world;
+    unsigned long long blocks = (unsigned long long)num_sms * per_sm;
+    if (blocks > units) blocks = units;
+    if (blocks == 0) return 0;
+    tile_kernel<W, XP><<<unsigned(blocks), kTileThreads, smem, st>>>(p, tp);
     return 1;
 }
 
@@ -795,20 +1142,24 @@ int launch_level_close(const ProblemDev &p, int g, long long lower, int from_key
     level_close_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, g, lower, from_keys);
     return 1;
 }
-size_t tile_smem_bytes(int G, int N, int W, int SW, int BK) { return tile_smem(G, N, W, SW, BK); }
+size_t tile_smem_bytes(int G, int N, int W, int K, int BK) { return tile_smem(G, N, W, K, BK); }
 
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool xp = p.K > p.W && p.W > 1;
+#define SDB_TILE_CASE(w)                                                                                 \
+    case w: return xp ? launch_tile_impl<w, true>(p, tp, st, num_sms) : launch_tile_impl<w, false>(p, tp, st, num_sms);
     switch (p.W) {
-        case 1: return launch_tile_impl<1>(p, tp, st, num_sms);
-        case 2: return launch_tile_impl<2>(p, tp, st, num_sms);
-        case 3: return launch_tile_impl<3>(p, tp, st, num_sms);
-        case 4: return launch_tile_impl<4>(p, tp, st, num_sms);
-        case 5: return launch_tile_impl<5>(p, tp, st, num_sms);
-        case 6: return launch_tile_impl<6>(p, tp, st, num_sms);
-        case 7: return launch_tile_impl<7>(p, tp, st, num_sms);
-        case 8: return launch_tile_impl<8>(p, tp, st, num_sms);
+        case 1: return launch_tile_impl<1, false>(p, tp, st, num_sms);
+        SDB_TILE_CASE(2)
+        SDB_TILE_CASE(3)
+        SDB_TILE_CASE(4)
+        SDB_TILE_CASE(5)
+        SDB_TILE_CASE(6)
+        SDB_TILE_CASE(7)
+        SDB_TILE_CASE(8)
     }
+#undef SDB_TILE_CASE
     return -1;
 }
 
@@ -860,6 +1211,32 @@ int launch_brute(const BruteDev &b, void *stream, int num_sms) {
         case 3: brute_kernel<3><<<unsigned(blocks), 256, 0, st>>>(b); return 1;
         case 4: brute_kernel<4><<<unsigned(blocks), 256, 0, st>>>(b); return 1;
     }
+    return -1;
+}
+
+size_t ptile_smem_bytes(int G, int N, int W, int K, int P, int E, int BKs) {
+    return ptile_layout(G, N, W, K, P, E, BKs).total;
+}
+
+int launch_ptile_level(const ProblemDev &p, const PkgDev &k, const PtileDev &d, const PTilePlan &tp, void *stream,
+                       int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool xp = p.K > p.W && p.W > 1;
+#define SDB_PTILE_CASE(w)                                                                                \
+    case w:                                                                                              \
+        return xp ? launch_ptile_impl<w, true>(p, k, d, tp, st, num_sms)                                 \
+                  : launch_ptile_impl<w, false>(p, k, d, tp, st, num_sms);
+    switch (p.W) {
+        case 1: return launch_ptile_impl<1, false>(p, k, d, tp, st, num_sms);
+        SDB_PTILE_CASE(2)
+        SDB_PTILE_CASE(3)
+        SDB_PTILE_CASE(4)
+        SDB_PTILE_CASE(5)
+        SDB_PTILE_CASE(6)
+        SDB_PTILE_CASE(7)
+        SDB_PTILE_CASE(8)
+    }
+#undef SDB_PTILE_CASE
     return -1;
 }
 
