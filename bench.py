@@ -405,6 +405,26 @@ def per_config(P, opts, torch):
     out["config3"] = {"codes": len(codes), "codes_per_s_e2e": len(codes) / res.elapsed_seconds,
                       "e2e_ms": 1e3 * res.elapsed_seconds, "device_ms": 1e3 * res.device_seconds,
                       "histogram": hist}
+    # the package routes on config 4, and the device brute force
+    c = P.CONFIGS[4]
+    a = P.generate_code(c["n"], c["k"], c["seed"])
+    for name in ("saved_1_gamma", "saved_2_gamma"):
+        fn = getattr(P, name)
+        fn(a, opts)
+        ts, r = [], None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            r = fn(a, opts)
+            ts.append(time.perf_counter() - t0)
+        out[f"config4_{name}"] = {"distance": r.distance, "trace": r.trace_tuples(), "candidates": r.candidates_enumerated,
+                                  "e2e_time_to_distance_ms": 1e3 * statistics.median(ts),
+                                  "device_levels_ms": 1e3 * r.enum_seconds,
+                                  "combos_per_s": r.candidates_enumerated / r.enum_seconds}
+    c = P.CONFIGS[1]
+    a = P.generate_code(c["n"], c["k"], c["seed"])
+    r = P.compute_distance(a, P.Algorithm.brute_force, opts)
+    out["config1_brute_force"] = {"distance": r.distance, "combinations": r.candidates_enumerated,
+                                  "device_ms": 1e3 * r.enum_seconds}
     c = P.CONFIGS[5]
     a = P.generate_code(c["n"], c["k"], c["seed"])
     o5 = P.RunOptions(device=opts.device, stream=opts.stream, max_generation=9)

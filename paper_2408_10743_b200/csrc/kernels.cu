@@ -538,7 +538,6 @@ __device__ __forceinline__ uint32_t probe_fold(const uint32_t (&hp)[K], const ui
     return u;
 }
 
-SDB_HD constexpr int probe_words(int W, bool XP) { return W == 1 ? 2 : W + (XP ? 1 : 0); }
 
 // colex successor of the ascending m-subset e (m >= 1) with the row sum kept in acc:
 // the lowest element that can move up by one moves, the ones below it reset to 0..q-1.
@@ -559,7 +558,8 @@ __device__ __forceinline__ void colex_step(int *e, int m, uint32_t (&acc)[NW], c
 }
 
 template <int W, bool XP>
-__global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W)) tile_kernel(ProblemDev p, TilePlan tp) {
+__global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W, XP)))
+    tile_kernel(ProblemDev p, TilePlan tp) {
     constexpr int H = heads_per_lane(W);
     constexpr int HB = head_block(W);
     constexpr int K = probe_words(W, XP);  // probe words per row / head / tail
@@ -866,7 +866,7 @@ __device__ __noinline__ unsigned ptile_exact(const ProblemDev p, const PkgDev k,
 }
 
 template <int W, bool XP>
-__global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W))
+__global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W, XP)))
     ptile_kernel(ProblemDev p, PkgDev k, PtileDev d, PTilePlan tp) {
     constexpr int H = heads_per_lane(W);
     constexpr int HB = head_block(W);
