@@ -48,10 +48,23 @@ static unsigned long long binom_u64(int a, int b) {
 }
 
 // bits of row r at columns [from, from+len) packed into u32 words
+// 64 bits of a row starting at column `from` (zero past the row's last word)
+static inline uint64_t row_bits64(const BitMat &m, int r, int from) {
+    const uint64_t *w = m.row(r);
+    const int wi = from >> 6, sh = from & 63;
+    const uint64_t lo = wi < m.stride ? w[wi] : 0, hi = (sh && wi + 1 < m.stride) ? w[wi + 1] : 0;
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+}
+
+// bits of row r at columns [from, from+len) packed into u32 words
 static void extract_bits(const BitMat &m, int r, int from, int len, uint32_t *dst, int words) {
     for (int i = 0; i < words; i++) dst[i] = 0;
-    for (int c = 0; c < len; c++)
-        if (m.get(r, from + c)) dst[c >> 5] |= 1u << (c & 31);
+    for (int c = 0; c < len; c += 64) {
+        uint64_t v = row_bits64(m, r, from + c);
+        if (len - c < 64) v &= (uint64_t(1) << (len - c)) - 1;
+        if ((c >> 5) < words) dst[c >> 5] = uint32_t(v);
+        if ((c >> 5) + 1 < words) dst[(c >> 5) + 1] = uint32_t(v >> 32);
+    }
 }
 
 ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
@@ -70,9 +83,9 @@ ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W)
         s ^= s >> 27;
         return s * 0x2545F4914F6CDD1Dull;
     };
-    const int g0 = std::min(N, 6), samples = 512;
+    const int g0 = std::min(N, 6), samples = 256;
     std::vector<uint32_t> acc(size_t(2 * W));
-    std::vector<std::vector<uint32_t>> sums(size_t(samples), std::vector<uint32_t>(size_t(2 * W)));
+    std::vector<uint32_t> sums(size_t(samples) * 2 * W);  // [sample][2W]
     ProbeChoice pc;
     pc.extra.assign(size_t(G), -1);
     double base_mean = 0, gain_mean = 0;
@@ -85,7 +98,7 @@ ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W)
                 const int r = int(next() % uint64_t(N));
                 for (int w = 0; w < 2 * W; w++) acc[size_t(w)] ^= base[size_t(r) * 2 * W + w];
             }
-            sums[size_t(smp)] = acc;
+            std::copy(acc.begin(), acc.end(), sums.begin() + long(smp) * 2 * W);
             for (int w = 0; w < W; w++) {
                 dx[size_t(w)] += __builtin_popcount(acc[size_t(w)]);
                 dz[size_t(w)] += __builtin_popcount(acc[size_t(W + w)]);
@@ -94,13 +107,15 @@ ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W)
         for (int w = 0; w < W; w++)
             if (dz[size_t(w)] > dx[size_t(w)]) {
                 for (int r = 0; r < N; r++) std::swap(base[size_t(r) * 2 * W + w], base[size_t(r) * 2 * W + W + w]);
-                for (auto &v : sums) std::swap(v[size_t(w)], v[size_t(W + w)]);
+                for (int smp = 0; smp < samples; smp++)
+                    std::swap(sums[size_t(smp) * 2 * W + w], sums[size_t(smp) * 2 * W + W + w]);
             }
         if (W == 1) continue;  // the fast path is exact already
         // mean fold weight with the probe words, and with each partner word added
         double fold = 0;
         std::vector<double> with(size_t(W), 0);
-        for (const auto &v : sums) {
+        for (int smp = 0; smp < samples; smp++) {
+            const uint32_t *v = sums.data() + size_t(smp) * 2 * W;
             uint32_t u = 0;
             for (int w = 0; w < W; w++) u |= v[size_t(w)];
             fold += __builtin_popcount(u);
@@ -200,12 +215,14 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
         sentinel_ = cols + 1;
         max_weight_ = cols;
         bool image = n > 0 && cols == 3 * n;
-        for (int j = 0; image && j < G_; j++)
-            for (int r = 0; image && r < N_; r++)
-                for (int i = 0; i < n; i++) {
-                    const BitMat &m = gammas_[size_t(j)].matrix;
-                    if (m.get(r, 2 * n + i) != (m.get(r, i) != m.get(r, n + i))) { image = false; break; }
+        for (int j = 0; image && j < G_; j++) {
+            const BitMat &m = gammas_[size_t(j)].matrix;
+            for (int r = 0; image && r < m.rows; r++)
+                for (int i = 0; i < n && image; i += 64) {
+                    const uint64_t mask = n - i >= 64 ? ~uint64_t(0) : ((uint64_t(1) << (n - i)) - 1);
+                    image = ((row_bits64(m, r, i) ^ row_bits64(m, r, n + i) ^ row_bits64(m, r, 2 * n + i)) & mask) == 0;
                 }
+        }
         image_layout_ = image;
         if (image) {
             W_ = (n + 31) / 32;
@@ -425,9 +442,9 @@ cudaStream_t thread_stream(int device) {
 }  // namespace
 
 Plan::~Plan() {
-    if (d_mem_ || h_pinned_) cudaStreamSynchronize(stream_);
+    if (d_mem_ || h_stage_) cudaStreamSynchronize(stream_);
     if (d_mem_) workspace_put(device_, d_bytes_, d_mem_);
-    if (h_pinned_) pinned_put(table_cap_ * 8, h_pinned_);
+    if (h_stage_) pinned_put(d_bytes_, h_stage_);
     for (cudaEvent_t e : events_)
         if (e) event_put(device_, e);
 }
@@ -456,64 +473,46 @@ void Plan::upload() {
                (packaged_ ? b_tables_pk + b_pkr + b_pks + b_ws + 4 * b_el + 2 * b_off + 2 * b_F : b_tables);
     const auto t0 = std::chrono::steady_clock::now();
     d_mem_ = workspace_get(device_, d_bytes_);
+    // every input section is laid out in one pinned staging image of the device block and
+    // goes over in a single asynchronous copy; the unit tables of later levels are staged in
+    // the same image (h_pinned_) and copied level by level
+    h_stage_ = static_cast<unsigned char *>(pinned_get(d_bytes_));
     unsigned char *base = static_cast<unsigned char *>(d_mem_);
-    check_cuda(cudaMemcpyAsync(base, h_rows_.data(), h_rows_.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D rows");
-    if (!h_syn_.empty())
-        check_cuda(cudaMemcpyAsync(base + b_rows, h_syn_.data(), h_syn_.size() * 8, cudaMemcpyHostToDevice, stream_),
-                   "H2D syn");
-    check_cuda(cudaMemcpyAsync(base + b_rows + b_syn, h_binom_.data(), h_binom_.size() * 8, cudaMemcpyHostToDevice,
-                               stream_),
-               "H2D binom");
+    size_t at = 0;
+    auto place = [&](const void *src, size_t bytes, size_t region) {
+        if (bytes) std::memcpy(h_stage_ + at, src, bytes);
+        unsigned char *dev = base + at;
+        at += region;
+        return dev;
+    };
+    pd_.rows = reinterpret_cast<const uint32_t *>(place(h_rows_.data(), h_rows_.size() * 4, b_rows));
+    pd_.syn = reinterpret_cast<const unsigned long long *>(place(h_syn_.data(), h_syn_.size() * 8, b_syn));
+    pd_.binom = reinterpret_cast<const unsigned long long *>(place(h_binom_.data(), h_binom_.size() * 8, b_binom));
     upload_bytes = h_rows_.size() * 4 + h_syn_.size() * 8 + h_binom_.size() * 8;
-    unsigned char *q = base + b_rows + b_syn + b_binom;
-    pd_.rows = reinterpret_cast<const uint32_t *>(base);
-    pd_.syn = reinterpret_cast<const unsigned long long *>(base + b_rows);
-    pd_.binom = reinterpret_cast<const unsigned long long *>(base + b_rows + b_syn);
+    unsigned char *q = place(nullptr, 0, b_state);
     pd_.state = reinterpret_cast<LevelState *>(q);
     pd_.key_by_w = reinterpret_cast<unsigned long long *>(q + sizeof(LevelState));
-    q += b_state;
-    pd_.ctl = reinterpret_cast<RunCtl *>(q);
-    q += b_ctl;
-    pd_.trace_upper = reinterpret_cast<int *>(q);
-    q += b_trace;
-    d_counters_ = reinterpret_cast<unsigned long long *>(q);
-    q += b_counters;
-    d_counter_init_ = reinterpret_cast<unsigned long long *>(q);
-    q += b_counters;
-    d_tables_ = reinterpret_cast<unsigned long long *>(q);
-    h_pinned_ = static_cast<unsigned long long *>(pinned_get(table_cap_ * 8));
-    q += packaged_ ? b_tables_pk : b_tables;
-    pd_.prows = reinterpret_cast<const uint32_t *>(q);
+    pd_.ctl = reinterpret_cast<RunCtl *>(place(nullptr, 0, b_ctl));
+    pd_.trace_upper = reinterpret_cast<int *>(place(nullptr, 0, b_trace));
+    d_counters_ = reinterpret_cast<unsigned long long *>(place(nullptr, 0, b_counters));
+    h_counter_init_.assign(size_t(N_ + 1), 0);
+    d_counter_init_ = reinterpret_cast<unsigned long long *>(place(h_counter_init_.data(), size_t(N_ + 1) * 8, b_counters));
+    h_pinned_ = reinterpret_cast<unsigned long long *>(h_stage_ + at);
+    d_tables_ = reinterpret_cast<unsigned long long *>(place(nullptr, 0, packaged_ ? b_tables_pk : b_tables));
+    pd_.prows = reinterpret_cast<const uint32_t *>(place(h_prows_.data(), h_prows_.size() * 4, b_prows));
     pd_.K = K_;
-    check_cuda(cudaMemcpyAsync(q, h_prows_.data(), h_prows_.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D probes");
-    q += b_prows;
     if (packaged_) {
-        pk_.pk_rows = reinterpret_cast<const short *>(q);
-        check_cuda(cudaMemcpyAsync(q, h_pk_rows_.data(), h_pk_rows_.size() * 2, cudaMemcpyHostToDevice, stream_),
-                   "H2D packages");
-        q += b_pkr;
-        pk_.pk_size = reinterpret_cast<const unsigned char *>(q);
-        check_cuda(cudaMemcpyAsync(q, h_pk_size_.data(), h_pk_size_.size(), cudaMemcpyHostToDevice, stream_),
-                   "H2D packages");
-        q += b_pks;
-        pk_.wsuf = reinterpret_cast<const unsigned long long *>(q);
-        check_cuda(cudaMemcpyAsync(q, h_wsuf_.data(), h_wsuf_.size() * 8, cudaMemcpyHostToDevice, stream_),
-                   "H2D packages");
-        q += b_ws;
-        auto put = [&](const void *src, size_t bytes, size_t region) {
-            check_cuda(cudaMemcpyAsync(q, src, bytes, cudaMemcpyHostToDevice, stream_), "H2D package tables");
-            unsigned char *at = q;
-            q += region;
-            return at;
-        };
-        pt_.e_row = reinterpret_cast<const short *>(put(h_e_row_.data(), h_e_row_.size() * 2, b_el));
-        pt_.e_pkg = reinterpret_cast<const short *>(put(h_e_pkg_.data(), h_e_pkg_.size() * 2, b_el));
-        pt_.r_row = reinterpret_cast<const short *>(put(h_r_row_.data(), h_r_row_.size() * 2, b_el));
-        pt_.r_pkg = reinterpret_cast<const short *>(put(h_r_pkg_.data(), h_r_pkg_.size() * 2, b_el));
-        pt_.off = reinterpret_cast<const short *>(put(h_off_.data(), h_off_.size() * 2, b_off));
-        pt_.r_off = reinterpret_cast<const short *>(put(h_r_off_.data(), h_r_off_.size() * 2, b_off));
-        pt_.F = reinterpret_cast<const unsigned long long *>(put(h_F_.data(), h_F_.size() * 8, b_F));
-        pt_.FR = reinterpret_cast<const unsigned long long *>(put(h_FR_.data(), h_FR_.size() * 8, b_F));
+        pk_.pk_rows = reinterpret_cast<const short *>(place(h_pk_rows_.data(), h_pk_rows_.size() * 2, b_pkr));
+        pk_.pk_size = reinterpret_cast<const unsigned char *>(place(h_pk_size_.data(), h_pk_size_.size(), b_pks));
+        pk_.wsuf = reinterpret_cast<const unsigned long long *>(place(h_wsuf_.data(), h_wsuf_.size() * 8, b_ws));
+        pt_.e_row = reinterpret_cast<const short *>(place(h_e_row_.data(), h_e_row_.size() * 2, b_el));
+        pt_.e_pkg = reinterpret_cast<const short *>(place(h_e_pkg_.data(), h_e_pkg_.size() * 2, b_el));
+        pt_.r_row = reinterpret_cast<const short *>(place(h_r_row_.data(), h_r_row_.size() * 2, b_el));
+        pt_.r_pkg = reinterpret_cast<const short *>(place(h_r_pkg_.data(), h_r_pkg_.size() * 2, b_el));
+        pt_.off = reinterpret_cast<const short *>(place(h_off_.data(), h_off_.size() * 2, b_off));
+        pt_.r_off = reinterpret_cast<const short *>(place(h_r_off_.data(), h_r_off_.size() * 2, b_off));
+        pt_.F = reinterpret_cast<const unsigned long long *>(place(h_F_.data(), h_F_.size() * 8, b_F));
+        pt_.FR = reinterpret_cast<const unsigned long long *>(place(h_FR_.data(), h_FR_.size() * 8, b_F));
         pt_.E = E_;
         pk_.P = P_;
         for (int j = 0; j < G_; j++) pk_.np[j] = np_[size_t(j)];
@@ -521,11 +520,8 @@ void Plan::upload() {
         if (pkg_smem_bytes(G_, N_, W_, SW_, P_, BK_) > 200 * 1024)
             throw InvalidArgument("problem too large for shared-memory staging");
     }
-    h_counter_init_.assign(size_t(N_ + 1), 0);
-    check_cuda(cudaMemcpyAsync(d_counter_init_, h_counter_init_.data(), size_t(N_ + 1) * 8, cudaMemcpyHostToDevice,
-                               stream_),
-               "H2D counters");
-    check_cuda(cudaStreamSynchronize(stream_), "H2D sync");
+    upload_bytes += h_prows_.size() * 4;
+    check_cuda(cudaMemcpyAsync(base, h_stage_, at, cudaMemcpyHostToDevice, stream_), "H2D plan");
     h2d_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     pd_.G = G_;
     pd_.N = N_;
@@ -826,7 +822,9 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     for (int g = 1; g <= g_limit; g++) {
         prepare_level(g);
         const LevelHost &lv = levels_[size_t(g)];
-        check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
+        // per-level events only when the caller wants per-level times; else one pair
+        // around all levels (fewer API calls on small codes)
+        if (level_seconds || g == 1) check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
         const int nl = lv.t == -2  ? launch_ptile_level(pd_, pk_, pt_, lv.ptile, stream_, num_sms_)
                        : lv.t == -1 ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
                        : lv.t == 0  ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
@@ -870,7 +868,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         }
         launches += launch_level_close(pd_, g, lower_bound(g), from_keys, stream_);
         check_cuda(cudaGetLastError(), "level close launch");
-        check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
+        if (level_seconds) check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
         last_g = g;
         const unsigned long long total = level_candidates(g);
         if ((lv.sharded && !opts_.comm) || total >= kSyncCandidates || g == g_limit) {
@@ -882,6 +880,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         if (!packaged_ && g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
             throw InvalidArgument("generation beyond the kernels' combination-size limit");
     }
+    if (!level_seconds) check_cuda(cudaEventRecord(level_event(1), stream_), "event");
     std::vector<int> tu(size_t(last_g + 1));
     check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
     check_cuda(cudaMemcpyAsync(tu.data(), pd_.trace_upper, tu.size() * 4, cudaMemcpyDeviceToHost, stream_), "D2H trace");
@@ -898,8 +897,10 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         U = tu[size_t(g)];
         const long long L = lower_bound(g);
         float ms = 0;
-        check_cuda(cudaEventElapsedTime(&ms, level_event(2 * g), level_event(2 * g + 1)), "event time");
-        enum_s += ms * 1e-3;
+        if (level_seconds) {
+            check_cuda(cudaEventElapsedTime(&ms, level_event(2 * g), level_event(2 * g + 1)), "event time");
+            enum_s += ms * 1e-3;
+        }
         candidates += level_candidates(g);
         generation = g;
         if (n_levels < trace_cap && trace) trace[n_levels] = sdb_trace_entry{g, L, U};
@@ -907,6 +908,11 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         n_levels++;
         if (L >= U) { complete = true; break; }
         if (g == (packaged_ ? *std::min_element(np_.begin(), np_.end()) : N_)) complete = true;
+    }
+    if (!level_seconds && last_g >= 1) {
+        float ms = 0;
+        check_cuda(cudaEventElapsedTime(&ms, level_event(2), level_event(1)), "event time");
+        enum_s = ms * 1e-3;
     }
     if (complete && U >= sentinel_)
         throw InternalFailure("run_bz: no admissible codeword after complete enumeration; "

@@ -98,7 +98,8 @@ class Plan {
     unsigned long long *d_tables_ = nullptr;    // tile unit tables of all levels, back to back
     size_t table_cap_ = 0, table_used_ = 0;
     std::vector<unsigned long long> h_counter_init_;
-    unsigned long long *h_pinned_ = nullptr;  // pinned staging of the unit tables (table_cap_ entries)
+    unsigned char *h_stage_ = nullptr;         // pinned staging image of the device block
+    unsigned long long *h_pinned_ = nullptr;  // its unit-table section (table_cap_ entries)
     // package routes
     bool packaged_ = false;
     int P_ = 0;                                  // package slots per Gamma

@@ -73,13 +73,31 @@ BitMat null_space(const BitMat &m) {
     return basis;
 }
 
+// 64 bits of row r from column `from` on (zero past the row)
+static inline uint64_t bits64(const BitMat &m, int r, int from) {
+    const uint64_t *w = m.row(r);
+    const int wi = from >> 6, sh = from & 63;
+    const uint64_t lo = wi < m.stride ? w[wi] : 0, hi = (sh && wi + 1 < m.stride) ? w[wi + 1] : 0;
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+}
+
+// OR `len` bits of v (low bits first) into row r at column `at`
+static inline void or_bits(BitMat &m, int r, int at, uint64_t v, int len) {
+    if (len < 64) v &= (uint64_t(1) << len) - 1;
+    uint64_t *w = m.row(r);
+    const int wi = at >> 6, sh = at & 63;
+    w[wi] |= v << sh;
+    if (sh && wi + 1 < m.stride) w[wi + 1] |= v >> (64 - sh);
+}
+
 static BitMat swap_halves(const BitMat &a) {
     const int n = a.cols / 2;
     BitMat s(a.rows, a.cols);
     for (int r = 0; r < a.rows; r++)
-        for (int i = 0; i < n; i++) {
-            if (a.get(r, n + i)) s.set(r, i, true);
-            if (a.get(r, i)) s.set(r, n + i, true);
+        for (int i = 0; i < n; i += 64) {
+            const int len = std::min(64, n - i);
+            or_bits(s, r, i, bits64(a, r, n + i), len);
+            or_bits(s, r, n + i, bits64(a, r, i), len);
         }
     return s;
 }
@@ -115,11 +133,12 @@ BitMat isometry_transform(const BitMat &a) {
     const int n = a.cols / 2;
     BitMat out(a.rows, 3 * n);
     for (int r = 0; r < a.rows; r++)
-        for (int i = 0; i < n; i++) {
-            const bool ai = a.get(r, i), bi = a.get(r, n + i);
-            if (ai) out.set(r, i, true);
-            if (bi) out.set(r, n + i, true);
-            if (ai != bi) out.set(r, 2 * n + i, true);
+        for (int i = 0; i < n; i += 64) {
+            const int len = std::min(64, n - i);
+            const uint64_t x = bits64(a, r, i), z = bits64(a, r, n + i);
+            or_bits(out, r, i, x, len);
+            or_bits(out, r, n + i, z, len);
+            or_bits(out, r, 2 * n + i, x ^ z, len);
         }
     return out;
 }
