@@ -131,6 +131,8 @@ ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W)
     // one more LOP3 per candidate pays only when the plain fold leaves the false-positive rate
     // high: its mean sits well below the 32 bits a word can show
     pc.use_extra = W > 1 && base_mean < 22.0 && gain_mean >= 2.0;
+    if (const char *force = std::getenv("SDB_EXTRA_PROBE"))  // experiments: 0 off, 1 on
+        pc.use_extra = W > 1 && force[0] == '1';
     return pc;
 }
 
