@@ -67,7 +67,7 @@ static void extract_bits(const BitMat &m, int r, int from, int len, uint32_t *ds
     }
 }
 
-ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W) {
+ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W, int bits) {
     // popc(x|z) is symmetric in x and z position by position, so swapping the x-word and
     // the z-word of one 32-symbol block (in every row of a Gamma) leaves every candidate
     // weight unchanged. The tile kernels' fast path folds the first (probe) word of each
@@ -88,6 +88,11 @@ ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W)
     std::vector<uint32_t> sums(size_t(samples) * 2 * W);  // [sample][2W]
     ProbeChoice pc;
     pc.extra.assign(size_t(G), -1);
+    pc.fill.assign(size_t(G), -1);
+    // the last block's unused bit positions: the fold may carry another block's partner
+    // component there (bit b then still tests only symbols at bit b of some block)
+    const int last = bits - 32 * (W - 1);
+    pc.free_mask = (W > 1 && last > 0 && last < 32) ? ~((1u << last) - 1u) : 0u;
     double base_mean = 0, gain_mean = 0;
     for (int j = 0; j < G; j++) {
         uint32_t *base = rows.data() + size_t(j) * N * 2 * W;
@@ -125,6 +130,21 @@ ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W)
         for (int e = 1; e < W; e++)
             if (with[size_t(e)] > with[size_t(best)]) best = e;
         pc.extra[size_t(j)] = best;
+        if (pc.free_mask) {
+            // which block's partner fills the free bits best
+            std::vector<double> fill(size_t(W - 1), 0);
+            for (int smp = 0; smp < samples; smp++) {
+                const uint32_t *v = sums.data() + size_t(smp) * 2 * W;
+                uint32_t u = 0;
+                for (int w = 0; w < W; w++) u |= v[size_t(w)];
+                for (int e = 0; e < W - 1; e++)
+                    fill[size_t(e)] += __builtin_popcount((u | (v[size_t(W + e)] & pc.free_mask)) & pc.free_mask);
+            }
+            int fb = 0;
+            for (int e = 1; e < W - 1; e++)
+                if (fill[size_t(e)] > fill[size_t(fb)]) fb = e;
+            pc.fill[size_t(j)] = fb;
+        }
         base_mean += fold / samples / G;
         gain_mean += (with[size_t(best)] - fold) / samples / G;
     }
@@ -257,7 +277,7 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
             }
         }
     lap("rows");
-    const ProbeChoice probe = orient_probe_words(h_rows_, G_, N_, W_);
+    const ProbeChoice probe = orient_probe_words(h_rows_, G_, N_, W_, image_layout_ ? n : 32 * W_);
     K_ = W_ == 1 ? 2 : W_ + (probe.use_extra ? 1 : 0);
     h_prows_.assign(size_t(G_) * N_ * K_, 0);
     for (int j = 0; j < G_; j++)
@@ -266,6 +286,7 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
             uint32_t *dst = h_prows_.data() + (size_t(j) * N_ + r) * K_;
             for (int w = 0; w < std::min(K_, W_ == 1 ? 2 : W_); w++) dst[w] = src[w];
             if (K_ > W_ && W_ > 1) dst[W_] = src[W_ + probe.extra[size_t(j)]];
+            if (probe.fill[size_t(j)] >= 0) dst[W_ - 1] |= src[W_ + probe.fill[size_t(j)]] & probe.free_mask;
         }
     lap("orient");
     SW_ = build_syndromes(gammas_, n, filter, h_syn_);

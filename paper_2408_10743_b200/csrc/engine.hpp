@@ -137,8 +137,11 @@ int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int 
 struct ProbeChoice {
     std::vector<int> extra;  // per Gamma: the block whose partner word may join the probe
     bool use_extra = false;  // probe words per row = W + 1 (else W; 2 when W = 1)
+    std::vector<int> fill;   // per Gamma: the block whose partner fills the last block's free bits
+    uint32_t free_mask = 0;  // bit positions of the last block that hold no symbol
 };
-ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W);
+// bits: symbols per half (the last block holds bits - 32 (W - 1) of them)
+ProbeChoice orient_probe_words(std::vector<uint32_t> &rows, int G, int N, int W, int bits);
 
 // Saturating binomial table (N+1) x BK.
 std::vector<unsigned long long> binom_table(int N, int BK);
