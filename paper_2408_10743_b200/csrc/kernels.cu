@@ -394,11 +394,14 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     const int g_last = b.max_g > 0 ? min(N, b.max_g) : N;
     for (int g = 1; g <= g_last; g++) {
         const unsigned long long per = binom_at(s_binom, b.BK, N, g);
-        // ~32 candidates per thread per segment keeps every thread busy on tiny levels
+        // one segment per thread: tiny levels get a candidate or two per thread, not a long
+        // serial walk on a few of them
         const unsigned long long total = per * G;
-        const unsigned long long seg_len = 32;
+        const unsigned long long seg_len = max(1ull, (total + blockDim.x - 1) / blockDim.x);
         const unsigned long long segs_per = (per + seg_len - 1) / seg_len;
-        unsigned int thr = unsigned(U - 1);
+        // thread-local minimum of the admissible candidates below U; one shared atomic per
+        // warp at the end instead of one per improving candidate
+        unsigned best = unsigned(U);
         for (unsigned long long seg = threadIdx.x; seg < segs_per * G; seg += blockDim.x) {
             const int j = int(seg / segs_per);
             const unsigned long long r0 = (seg % segs_per) * seg_len;
@@ -413,10 +416,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
             unsigned long long r = r0;
             for (;;) {
                 const unsigned int w = unsigned(b.scale * weight_of<W>(acc));
-                if (w <= thr && admissible_combo(syn, b.SW, c, g)) {
-                    atomicMin(&s_wmin, w);
-                    thr = w;
-                }
+                if (w < best && admissible_combo(syn, b.SW, c, g)) best = w;
                 if (++r >= r1) break;
                 int i = g - 1;
                 while (c[i] == N - g + i) i--;
@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
                 for (int m = i; m < g; m++) xor_row<W>(acc, rows + c[m] * rowlen);
             }
         }
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_down_sync(0xffffffffu, best, o));
+        if ((threadIdx.x & 31) == 0 && best < unsigned(U)) atomicMin(&s_wmin, best);
         (void)total;
         __syncthreads();
         if (threadIdx.x == 0) {
