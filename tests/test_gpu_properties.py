@@ -113,3 +113,16 @@ def test_nccl_exchange_path_on_one_gpu(gpu):
         assert g2.distance == base.distance
     finally:
         comm.close()
+
+
+def test_config5_through_g10_matches_the_full_run(gpu):
+    # levels g <= 8 are pinned to the reference (config5_g8.json); g = 9, 10 against this
+    # build's own complete run (profiles/r01_config5_full.json: d = 14 after 13 levels), which
+    # no CPU can reproduce (SURVEY.md §0 finding 3) — a determinism and monotonicity check
+    c = gpu.CONFIGS[5]
+    a = gpu.generate_code(c["n"], c["k"], c["seed"])
+    rep = gpu.saved_isometry(a, gpu.RunOptions(max_generation=10))
+    full = [(1, 4, 44), (2, 6, 42), (3, 8, 36), (4, 10, 34), (5, 12, 32), (6, 14, 30), (7, 16, 30), (8, 18, 28),
+            (9, 20, 28), (10, 22, 28)]
+    assert tr(rep) == full
+    assert rep.candidates_visited == rep.candidates_enumerated == 19537662444573
