@@ -24,14 +24,14 @@ namespace {
 
 // Opt a kernel into up to 200 KB of dynamic shared memory, once per device (the attribute
 // is per device; a process may drive several GPUs).
-template <class Kernel>
-void allow_big_smem(Kernel kernel) {
-    static std::atomic<unsigned long long> done{0};
+template <auto Kernel>
+void allow_big_smem() {
+    static std::atomic<unsigned long long> done{0};  // one per kernel (Kernel is a value)
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (done.load(std::memory_order_acquire) & bit) return;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
@@ -316,7 +316,7 @@ template <int W>
 int launch_pkg_impl(const ProblemDev &p, const PkgDev &k, const PkgLevel &L, cudaStream_t st, int num_sms) {
     size_t a, b, c, d;
     const size_t smem = pkg_layout(p.G, p.N, W, p.SW, k.P, p.BK, &a, &b, &c, &d);
-    allow_big_smem(pkg_kernel<W>);
+    allow_big_smem<pkg_kernel<W>>();
     const unsigned long long segs = (L.seg_total + L.shard_world - 1 - L.shard_rank) / L.shard_world;
     unsigned long long blocks = (segs + 255) / 256;
     const unsigned long long cap = (unsigned long long)num_sms * 8;
@@ -1069,7 +1069,7 @@ template <int W, bool XP>
 int launch_ptile_impl(const ProblemDev &p, const PkgDev &k, const PtileDev &d, const PTilePlan &tp, cudaStream_t st,
                       int num_sms) {
     const size_t smem = ptile_layout(p.G, p.N, W, probe_words(W, XP), k.P, d.E, min(p.BK, tp.g + 2)).total;
-    allow_big_smem(ptile_kernel<W, XP>);
+    allow_big_smem<ptile_kernel<W, XP>>();
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ptile_kernel<W, XP>, kTileThreads, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1086,7 +1086,7 @@ size_t tile_smem(int G, int N, int W, int K, int BK) { return tile_smem_layout(G
 template <int W, bool XP>
 int launch_tile_impl(const ProblemDev &p, const TilePlan &tp, cudaStream_t st, int num_sms) {
     const size_t smem = tile_smem(p.G, p.N, W, probe_words(W, XP), min(p.BK, tp.g + 2));
-    allow_big_smem(tile_kernel<W, XP>);
+    allow_big_smem<tile_kernel<W, XP>>();
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<W, XP>, kTileThreads, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1105,7 +1105,7 @@ size_t problem_smem(int G, int N, int W, int SW, int BK) {
 template <int W>
 int launch_walk_impl(const ProblemDev &p, const LevelLaunch &L, cudaStream_t st, int num_sms) {
     const size_t smem = problem_smem(p.G, p.N, W, p.SW, p.BK);
-    allow_big_smem(walk_kernel<W>);
+    allow_big_smem<walk_kernel<W>>();
     const unsigned long long segs = (L.seg_total + L.shard_world - 1 - L.shard_rank) / L.shard_world;
     const int threads = 256;
     unsigned long long blocks = (segs + threads - 1) / threads;
@@ -1119,7 +1119,7 @@ int launch_walk_impl(const ProblemDev &p, const LevelLaunch &L, cudaStream_t st,
 template <int W>
 int launch_batch_impl(const BatchDev &b, cudaStream_t st) {
     const size_t smem = problem_smem(b.G, b.N, W, b.SW, b.BK);
-    allow_big_smem(batch_kernel<W>);
+    allow_big_smem<batch_kernel<W>>();
     batch_kernel<W><<<b.codes, 256, smem, st>>>(b);
     return 1;
 }
