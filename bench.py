@@ -332,7 +332,7 @@ def run_ours(args):
                             f"{c['seed']} (BASELINE.md §2 xorshift64* transvection generator)",
                 "n": c["n"], "k": c["k"], "seed": c["seed"], "distance": r0.distance,
                 "trace": r0.trace_tuples(), "candidates_per_step": cands, "levels": len(r0.bounds_trace),
-                "parallelism": (f"rank-space shard x{world} (levels >= 2^24 candidates; NCCL min-allreduce of the "
+                "parallelism": (f"rank-space shard x{world} (levels >= 2^26 candidates; NCCL min-allreduce of the "
                                 f"per-weight keys per sharded level)" if world > 1 else "single GPU"), "l2": "flushed (256 MB write) before every timed step",
                 "time_to_distance_ms": {"device_levels": total_ms / args.steps, "e2e_c_abi": e2e_ms / args.steps},
             },

@@ -110,7 +110,7 @@ typedef struct {
     void *comm;             /* sdb_comm_create handle (NCCL): with world > 1 the level exchange is a
                                stream-ordered min-allreduce, no host round trip (else allreduce_min) */
     long long shard_min;    /* levels with fewer candidates run whole on every rank, no exchange
-                               (0: default 2^24; 1: shard every level) */
+                               (0: default 2^26; 1: shard every level) */
     int reserved[4];
 } sdb_run_options;
 

@@ -248,7 +248,7 @@ class RunOptions:
     kernel: int = 0  # 0 auto, 1 walk, 2 tile
     stream: int = 0  # cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream); 0 = private
     comm: int = 0  # Comm.handle (NCCL): the level exchange runs on the stream, no host round trip
-    shard_min: int = 0  # levels below this many candidates run whole on every rank (0: 2^24)
+    shard_min: int = 0  # levels below this many candidates run whole on every rank (0: 2^26)
 
     def _c(self) -> tuple[_Options, object]:
         o = _Options()

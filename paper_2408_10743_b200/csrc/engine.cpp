@@ -601,7 +601,10 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
                 biggest = std::max(biggest, nH > 1 ? unit_full : unit_last);
             }
             sum *= G;
-            const double time = std::max(sum / slots, biggest);
+            // the average load per CTA slot plus the tail: the last units finish unevenly,
+            // about half the biggest unit late on average (this matters when sharding leaves
+            // few units per CTA)
+            const double time = std::max(sum / slots + 0.5 * biggest, biggest);
             if (time < best_time) {
                 best_time = time;
                 best = TileChoice{t, tchunk};
@@ -665,7 +668,10 @@ bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
                     sum += nT * ((nH - 1) * unit_full + unit_last);
                     biggest = std::max(biggest, nH > 1 ? unit_full : unit_last);
                 }
-            const double time = std::max(sum / slots, biggest);
+            // the average load per CTA slot plus the tail: the last units finish unevenly,
+            // about half the biggest unit late on average (this matters when sharding leaves
+            // few units per CTA)
+            const double time = std::max(sum / slots + 0.5 * biggest, biggest);
             if (time < best_time) {
                 best_time = time;
                 best_t = t;
@@ -751,7 +757,8 @@ void Plan::prepare_level(int g) {
             total += L.total[j];
         }
         const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
-        L.seg_len = std::max<unsigned long long>(1, (total + threads_total - 1) / threads_total);
+        const unsigned long long threads_all = threads_total * (unsigned long long)world;
+        L.seg_len = std::max<unsigned long long>(1, (total + threads_all - 1) / threads_all);
         L.seg_total = 0;
         for (int j = 0; j < G_; j++) {
             L.segs[j] = (L.total[j] + L.seg_len - 1) / L.seg_len;
@@ -776,7 +783,8 @@ void Plan::prepare_level(int g) {
         const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
         // one segment per thread of the full grid: tiny levels get one candidate per thread
         // instead of a long serial walk on a few threads
-        LL.seg_len = std::max<unsigned long long>(1, (total + threads_total - 1) / threads_total);
+        const unsigned long long threads_all = threads_total * (unsigned long long)world;  // every rank's grid
+        LL.seg_len = std::max<unsigned long long>(1, (total + threads_all - 1) / threads_all);
         LL.segs_per_gamma = (per + LL.seg_len - 1) / LL.seg_len;
         const unsigned long long S = LL.segs_per_gamma * (unsigned long long)G_;
         LL.seg_total = S;
@@ -815,6 +823,12 @@ void Plan::prepare_level(int g) {
         if (tile_smem_bytes(G_, N_, W_, K_, std::min(BK_, g + 2)) > 200 * 1024)
             throw InvalidArgument("problem too large for shared-memory staging");
     }
+    if (std::getenv("SDB_TRACE_HOST"))
+        std::fprintf(stderr, "[sdb] level %d: %s t=%d tchunk=%d units=%llu segs=%llu seg_len=%llu sharded=%d\n", g,
+                     lv.t ? "tile" : "walk", lv.t, lv.t ? lv.tile.tchunk : 0,
+                     lv.t ? (unsigned long long)lv.tile.unit_total : 0ull,
+                     lv.t ? 0ull : (unsigned long long)lv.walk.seg_total, lv.t ? 0ull : (unsigned long long)lv.walk.seg_len,
+                     int(lv.sharded));
     lv.ready = true;
 }
 

@@ -128,7 +128,7 @@ struct TileChoice {
 TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
                        int world);
 // levels with fewer candidates run whole on every rank (RunOptions.shard_min = 0)
-constexpr unsigned long long kDefaultShardMin = 1ull << 24;
+constexpr unsigned long long kDefaultShardMin = 1ull << 26;
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel);
 
 // Per Gamma and 32-symbol block, swap the x- and z-words of every row so that the word the
