@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "device.hpp"
@@ -18,6 +19,8 @@ enum class Mode { symplectic = 0, hamming = 1 };
 
 // One prepared matrix (singleton packages, prep.hpp:25-35 with packages[i] = {pivot, {i}}).
 struct GammaIn {
+    GammaIn() = default;
+    GammaIn(BitMat m, int deficit) : matrix(std::move(m)), rank_deficit(deficit) {}
     BitMat matrix;
     int rank_deficit = 0;
     // package routes: member rows of each package (1 or 3 rows); empty = every row is its
