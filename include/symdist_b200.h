@@ -104,8 +104,10 @@ typedef struct {
     int world;              /* number of shards (GPUs); 1 = single GPU */
     sdb_allreduce_min_fn allreduce_min;
     void *allreduce_ctx;
-    int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel, 2 force the tile kernel,
-                               3 batch only: run the prep (validation, information sets) on the host */
+    int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel (batch: every level on
+                               the per-thread walk, no meet-in-the-middle lists), 2 force the tile
+                               kernel, 3 batch only: run the prep (validation, information sets) on
+                               the host */
     void *stream;           /* cudaStream_t to run on (NULL: a private non-blocking stream) */
     void *comm;             /* sdb_comm_create handle (NCCL): with world > 1 the level exchange is a
                                stream-ordered min-allreduce, no host round trip (else allreduce_min) */

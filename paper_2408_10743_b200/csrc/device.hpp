@@ -240,7 +240,13 @@ struct BatchDev {
     int codes, G, N, W, SW, BK, scale, sentinel;
     int Gs;                    // Gamma slots per code in rows/syn/deficits (>= G)
     int max_g;                 // last level to run (RunOptions.max_generation; N when 0)
+    const int *n_gammas;       // [codes] matrices per code (device prep) or null: G for all
+    int threads;               // CTA size (a multiple of 32; 0 = 256)
+    int no_mitm;               // 1: every level on the per-thread walk (tests)
+    int mitm_g, mitm_cap;      // set by the launcher: meet-in-the-middle levels and list entries
 };
+// out_status of a code whose prep produced more matrices than the batch has slots
+constexpr int kBatchNeedsHostPrep = 5;
 int launch_batch(const BatchDev &b, void *stream);
 
 // Batch prep on the device, one warp per code (BASELINE config 3):

@@ -1079,50 +1079,69 @@ int run_brute(const BitMat &a, const sdb_run_options &o, double *device_seconds)
 // Batch with the prep on the device (one warp per code). Returns false, having written
 // nothing, when some code needs more Gamma slots than the prep kernel keeps (the caller then
 // runs the host-prep path).
-static bool run_batch_device(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words,
+// Device path of the batch: prep and the level loops both on the device, one H2D of the
+// normalizers (with the binomial table) from pinned staging, one D2H of every result, and no
+// host round trip in between (each code reads its own matrix count from the prep).
+static void run_batch_device(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words,
                              const sdb_run_options &o, int *distances, int *statuses, int *generations,
-                             sdb_trace_entry *traces, int *trace_lens, int trace_cap, double *device_seconds) {
+                             sdb_trace_entry *traces, int *trace_lens, int trace_cap, double *device_seconds,
+                             std::vector<int> &host_prep) {
     const int n = n_cols / 2, k = n_rows - n, N = n_rows, W = (n + 31) / 32;
     const int Gs = kPrepGammaSlots, SW = (o.dual_filter && k >= 1) ? 1 : 0, BK = std::min(N, kMaxLevel) + 2;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     check_cuda(cudaSetDevice(o.device), "cudaSetDevice");
     cudaStream_t st = o.stream ? static_cast<cudaStream_t>(o.stream) : thread_stream(o.device);
     const std::vector<unsigned long long> h_binom = binom_table(N, BK);
     const size_t nc = size_t(n_codes);
-    const size_t b_in = align256(nc * N * row_words * 8), b_rows = align256(nc * Gs * N * 2 * W * 4),
+    const size_t in_bytes = nc * N * row_words * 8, binom_bytes = h_binom.size() * 8;
+    const size_t b_in = align256(in_bytes), b_binom = align256(binom_bytes), b_rows = align256(nc * Gs * N * 2 * W * 4),
                  b_syn = align256(std::max<size_t>(nc * Gs * N * SW, 1) * 8), b_def = align256(nc * Gs * 4),
-                 b_int = align256(nc * 4), b_binom = align256(h_binom.size() * 8), b_tr = align256(nc * N * 4);
-    const size_t bytes = b_in + b_rows + b_syn + b_def + 5 * b_int + b_binom + 2 * b_tr;
+                 b_int = align256(nc * 4), b_tr = align256(nc * N * 4);
+    const size_t b_up = b_in + b_binom, b_out = 3 * b_int + 2 * b_tr;
+    const size_t bytes = b_up + b_rows + b_syn + b_def + 2 * b_int + b_out;
     void *mem = workspace_get(o.device, bytes);
+    unsigned char *h_up = static_cast<unsigned char *>(pinned_get(b_up));
+    unsigned char *h_out = static_cast<unsigned char *>(pinned_get(b_out));
+    cudaEvent_t e0 = event_get(o.device), e1 = event_get(o.device);
     struct Release {
         int dev;
-        size_t bytes;
+        size_t bytes, b_up, b_out;
         void *p;
+        unsigned char *h_up, *h_out;
+        cudaEvent_t e0, e1;
         cudaStream_t st;
         ~Release() {
             cudaStreamSynchronize(st);
             workspace_put(dev, bytes, p);
+            pinned_put(b_up, h_up);
+            pinned_put(b_out, h_out);
+            event_put(dev, e0);
+            event_put(dev, e1);
         }
-    } release{o.device, bytes, mem, st};
+    } release{o.device, bytes, b_up, b_out, mem, h_up, h_out, e0, e1, st};
     unsigned char *q = static_cast<unsigned char *>(mem);
     auto take = [&q](size_t b) {
         unsigned char *p = q;
         q += b;
         return p;
     };
+    unsigned char *d_up = take(b_up);
     BatchPrepDev pd{};
-    pd.normalizers = reinterpret_cast<const unsigned long long *>(take(b_in));
+    pd.normalizers = reinterpret_cast<const unsigned long long *>(d_up);
     pd.rows = reinterpret_cast<uint32_t *>(take(b_rows));
     pd.syn = reinterpret_cast<unsigned long long *>(take(b_syn));
     pd.deficits = reinterpret_cast<int *>(take(b_def));
     pd.n_gammas = reinterpret_cast<int *>(take(b_int));
     pd.status = reinterpret_cast<int *>(take(b_int));
+    unsigned char *d_out = take(b_out);
     BatchDev bd{};
-    bd.out_upper = reinterpret_cast<int *>(take(b_int));
-    bd.out_generations = reinterpret_cast<int *>(take(b_int));
-    bd.out_status = reinterpret_cast<int *>(take(b_int));
-    bd.binom = reinterpret_cast<const unsigned long long *>(take(b_binom));
-    bd.out_trace_lower = reinterpret_cast<int *>(take(b_tr));
-    bd.out_trace_upper = reinterpret_cast<int *>(take(b_tr));
+    bd.binom = reinterpret_cast<const unsigned long long *>(d_up + b_in);
+    bd.out_upper = reinterpret_cast<int *>(d_out);
+    bd.out_generations = reinterpret_cast<int *>(d_out + b_int);
+    bd.out_status = reinterpret_cast<int *>(d_out + 2 * b_int);
+    bd.out_trace_lower = reinterpret_cast<int *>(d_out + 3 * b_int);
+    bd.out_trace_upper = reinterpret_cast<int *>(d_out + 3 * b_int + b_tr);
     pd.in_words = row_words;
     pd.codes = n_codes;
     pd.N = N;
@@ -1131,81 +1150,77 @@ static bool run_batch_device(const uint64_t *rows, int n_codes, int n_rows, int 
     pd.validate = o.validate;
     pd.filter = SW;
     pd.Gs = Gs;
-    check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(pd.normalizers), rows, nc * N * row_words * 8,
-                               cudaMemcpyHostToDevice, st),
-               "H2D normalizers");
-    check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(bd.binom), h_binom.data(), h_binom.size() * 8,
-                               cudaMemcpyHostToDevice, st),
-               "H2D binom");
-    cudaEvent_t e0 = event_get(o.device), e1 = event_get(o.device);
+    const auto t1 = clk::now();
+    std::memcpy(h_up, rows, in_bytes);
+    std::memcpy(h_up + b_in, h_binom.data(), binom_bytes);
+    const auto t2 = clk::now();
+    check_cuda(cudaMemcpyAsync(d_up, h_up, b_up, cudaMemcpyHostToDevice, st), "H2D normalizers");
     check_cuda(cudaEventRecord(e0, st), "event");
     launch_batch_prep(pd, st);
     check_cuda(cudaGetLastError(), "batch prep launch");
-    std::vector<int> ng(nc), pst(nc);
-    check_cuda(cudaMemcpyAsync(ng.data(), pd.n_gammas, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    check_cuda(cudaMemcpyAsync(pst.data(), pd.status, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    check_cuda(cudaStreamSynchronize(st), "batch prep sync");
-    int G = 0;
-    for (size_t c = 0; c < nc; c++)
-        if (pst[c] == 0) G = std::max(G, ng[c]);
-    if (G > Gs) {
-        event_put(o.device, e0);
-        event_put(o.device, e1);
-        return false;
-    }
+    bd.rows = pd.rows;
+    bd.syn = pd.syn;
+    bd.deficits = pd.deficits;
+    bd.in_status = pd.status;
+    bd.n_gammas = pd.n_gammas;
+    bd.codes = n_codes;
+    bd.G = Gs;
+    bd.Gs = Gs;
+    bd.N = N;
+    bd.W = W;
+    bd.SW = SW;
+    bd.BK = BK;
+    bd.scale = 2;
+    bd.sentinel = 3 * n + 1;
+    bd.max_g = o.max_generation;
+    // enough resident codes per SM to cover the per-code level barriers
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+    bd.threads = n_codes >= 4 * sms ? 128 : 256;
+    bd.no_mitm = o.kernel == 1;
+    if (problem_smem_bytes(Gs, N, W, SW, BK) > 200 * 1024) throw InvalidArgument("batch codes too large");
+    if (launch_batch(bd, st) < 0) throw InvalidArgument("unsupported row width");
+    check_cuda(cudaGetLastError(), "batch kernel launch");
+    check_cuda(cudaEventRecord(e1, st), "event");
+    check_cuda(cudaMemcpyAsync(h_out, d_out, b_out, cudaMemcpyDeviceToHost, st), "D2H results");
+    const auto t3 = clk::now();
+    check_cuda(cudaStreamSynchronize(st), "batch sync");
+    const auto t4 = clk::now();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (device_seconds) *device_seconds = ms * 1e-3;
+    const int *up = reinterpret_cast<const int *>(h_out), *gen = reinterpret_cast<const int *>(h_out + b_int),
+              *stt = reinterpret_cast<const int *>(h_out + 2 * b_int),
+              *tl = reinterpret_cast<const int *>(h_out + 3 * b_int),
+              *tu = reinterpret_cast<const int *>(h_out + 3 * b_int + b_tr);
     for (int c = 0; c < n_codes; c++) {
+        const size_t cc = size_t(c);
         distances[c] = -1;
         generations[c] = 0;
         trace_lens[c] = 0;
-        statuses[c] = pst[size_t(c)] == 0 ? 0 : SDB_ERR_VALIDATION;
-    }
-    if (G > 0) {
-        bd.rows = pd.rows;
-        bd.syn = pd.syn;
-        bd.deficits = pd.deficits;
-        bd.in_status = pd.status;
-        bd.codes = n_codes;
-        bd.G = G;
-        bd.Gs = Gs;
-        bd.N = N;
-        bd.W = W;
-        bd.SW = SW;
-        bd.BK = BK;
-        bd.scale = 2;
-        bd.sentinel = 3 * n + 1;
-        bd.max_g = o.max_generation;
-        if (problem_smem_bytes(G, N, W, SW, BK) > 200 * 1024) throw InvalidArgument("batch codes too large");
-        if (launch_batch(bd, st) < 0) throw InvalidArgument("unsupported row width");
-        check_cuda(cudaGetLastError(), "batch kernel launch");
-        check_cuda(cudaEventRecord(e1, st), "event");
-        std::vector<int> up(nc), gen(nc), stt(nc), tl(nc * N), tu(nc * N);
-        check_cuda(cudaMemcpyAsync(up.data(), bd.out_upper, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        check_cuda(cudaMemcpyAsync(gen.data(), bd.out_generations, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        check_cuda(cudaMemcpyAsync(stt.data(), bd.out_status, nc * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        check_cuda(cudaMemcpyAsync(tl.data(), bd.out_trace_lower, nc * N * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        check_cuda(cudaMemcpyAsync(tu.data(), bd.out_trace_upper, nc * N * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        check_cuda(cudaStreamSynchronize(st), "batch sync");
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        if (device_seconds) *device_seconds = ms * 1e-3;
-        for (int c = 0; c < n_codes; c++) {
-            if (statuses[c] != 0) continue;
-            const size_t cc = size_t(c);
-            generations[c] = gen[cc];
-            trace_lens[c] = gen[cc];
-            for (int g = 0; g < gen[cc] && g < trace_cap; g++)
-                traces[cc * trace_cap + g] = sdb_trace_entry{g + 1, tl[cc * N + g], tu[cc * N + g]};
-            if (stt[cc] != 0 || up[cc] % 2 != 0)
-                statuses[c] = SDB_ERR_INTERNAL;
-            else
-                distances[c] = up[cc] / 2;
+        statuses[c] = 0;
+        if (stt[cc] == kBatchNeedsHostPrep) {
+            host_prep.push_back(c);
+            continue;
         }
-    } else if (device_seconds) {
-        *device_seconds = 0;
+        if (stt[cc] == 2) {  // the prep's validation / information_sets failure
+            statuses[c] = SDB_ERR_VALIDATION;
+            continue;
+        }
+        generations[c] = gen[cc];
+        trace_lens[c] = gen[cc];
+        for (int g = 0; g < gen[cc] && g < trace_cap; g++)
+            traces[cc * trace_cap + g] = sdb_trace_entry{g + 1, tl[cc * N + g], tu[cc * N + g]};
+        if (stt[cc] != 0 || up[cc] % 2 != 0)
+            statuses[c] = SDB_ERR_INTERNAL;
+        else
+            distances[c] = up[cc] / 2;
     }
-    event_put(o.device, e0);
-    event_put(o.device, e1);
-    return true;
+    if (std::getenv("SDB_TRACE_HOST")) {
+        auto ms = [](clk::time_point a, clk::time_point b) { return 1e3 * std::chrono::duration<double>(b - a).count(); };
+        std::fprintf(stderr, "[sdb] batch: setup %.3f, stage %.3f, launch %.3f, wait %.3f, unpack %.3f ms\n", ms(t0, t1),
+                     ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, clk::now()));
+    }
 }
 
 void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int row_words, const sdb_run_options &o,
@@ -1227,10 +1242,35 @@ void run_batch(const uint64_t *rows, int n_codes, int n_rows, int n_cols, int ro
             if (device_seconds) *device_seconds = 0;
             return;
         }
-        if (o.kernel != 3 && n_rows >= 1 && n_rows <= kPrepMaxRows && n <= kPrepMaxN &&
+        if (o.kernel != 3 && n_rows >= 1 && n_rows <= kPrepMaxRows && n <= kPrepMaxN) {
+            std::vector<int> redo;
             run_batch_device(rows, n_codes, n_rows, n_cols, row_words, o, distances, statuses, generations, traces,
-                             trace_lens, trace_cap, device_seconds))
+                             trace_lens, trace_cap, device_seconds, redo);
+            if (redo.empty()) return;
+            // codes with more information sets than the device prep has slots: host prep
+            std::vector<uint64_t> sub(redo.size() * size_t(n_rows) * size_t(row_words));
+            for (size_t i = 0; i < redo.size(); i++)
+                std::memcpy(sub.data() + i * n_rows * row_words, rows + size_t(redo[i]) * n_rows * row_words,
+                            size_t(n_rows) * row_words * 8);
+            const size_t m = redo.size();
+            std::vector<int> d(m), s(m), g(m), tl(m);
+            std::vector<sdb_trace_entry> tr(m * size_t(std::max(trace_cap, 1)));
+            sdb_run_options oh = o;
+            oh.kernel = 3;
+            double dev2 = 0;
+            run_batch(sub.data(), int(m), n_rows, n_cols, row_words, oh, d.data(), s.data(), g.data(), tr.data(),
+                      tl.data(), trace_cap, &dev2);
+            for (size_t i = 0; i < m; i++) {
+                const int c = redo[i];
+                distances[c] = d[i];
+                statuses[c] = s[i];
+                generations[c] = g[i];
+                trace_lens[c] = tl[i];
+                for (int e = 0; e < trace_cap; e++) traces[size_t(c) * trace_cap + e] = tr[i * trace_cap + e];
+            }
+            if (device_seconds) *device_seconds += dev2;
             return;
+        }
     }
     if (n_cols % 2 != 0 || n_cols == 0)
         throw InvalidArgument("StabilizerInstance: column count must be even and nonzero");

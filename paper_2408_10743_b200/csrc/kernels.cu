@@ -367,21 +367,191 @@ __global__ void __launch_bounds__(256) brute_kernel(BruteDev b) {
 
 // ---------------------------------------------------------------- batch: one code per CTA
 
+// Meet-in-the-middle levels of the batch kernel. The rows of one matrix split into halves
+// A = [0, nA) and B = [nA, N); list L_h of a half holds the XOR sums (and syndromes) of its
+// h-subsets in colex order, so the g-combinations are exactly the pairs A_h x B_(g-h),
+// h = 0..g. A warp fixes one entry of the shorter list and its lanes stride the longer one:
+// every candidate is one shared load, the XORs and a POPC per word, with no divergence.
+template <int W>
+struct MitmEnt;
+template <>
+struct MitmEnt<1> {
+    using T = uint2;
+    static __device__ __forceinline__ T zero() { return make_uint2(0u, 0u); }
+    static __device__ __forceinline__ T load_row(const uint32_t *r) { return make_uint2(r[0], r[1]); }
+    static __device__ __forceinline__ T x(T a, T b) { return make_uint2(a.x ^ b.x, a.y ^ b.y); }
+    static __device__ __forceinline__ unsigned weight(T a, T b) { return __popc((a.x ^ b.x) | (a.y ^ b.y)); }
+};
+template <>
+struct MitmEnt<2> {
+    using T = uint4;  // (x0, x1, z0, z1)
+    static __device__ __forceinline__ T zero() { return make_uint4(0u, 0u, 0u, 0u); }
+    static __device__ __forceinline__ T load_row(const uint32_t *r) { return make_uint4(r[0], r[1], r[2], r[3]); }
+    static __device__ __forceinline__ T x(T a, T b) { return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w); }
+    static __device__ __forceinline__ unsigned weight(T a, T b) {
+        return __popc((a.x ^ b.x) | (a.z ^ b.z)) + __popc((a.y ^ b.y) | (a.w ^ b.w));
+    }
+};
+
+// matrices whose lists stay resident (the per-matrix stride is sized for this many)
+constexpr int kMitmSlots = 3;
+
+// first entry of L_h in an n-element half: sum of C(n, s), s < h
+__device__ __forceinline__ int mitm_off(const unsigned long long *binom, int BK, int n, int h) {
+    int e = 0;
+    for (int s = 0; s < h; s++) e += int(binom[n * BK + s]);
+    return e;
+}
+
+// colex unrank of entry e of L_h of a half into the XOR of the syndromes of its elements
+__device__ __forceinline__ unsigned long long mitm_syndrome(const unsigned long long *binom, int BK, int n, int h,
+                                                            int e, const unsigned long long *syn) {
+    unsigned long long x = 0;
+    int m = n - 1;
+    for (int i = h; i >= 1; i--) {
+        while (binom[m * BK + i] > (unsigned long long)e) m--;
+        x ^= syn[m];
+        e -= int(binom[m * BK + i]);
+        m--;
+    }
+    return x;
+}
+
+// L_g of both halves of every matrix (and L_0 at g = 1), from the resident L_(g-1):
+// in colex order the g-subsets with maximum m follow those with maximum < m, and their first
+// g - 1 elements are the first C(m, g-1) entries of L_(g-1)
+template <int W>
+__device__ __forceinline__ void mitm_build(int g, int G, int N, const uint32_t *s_rows, const unsigned long long *binom,
+                                           int BK, typename MitmEnt<W>::T *ent, int blockB, int stride) {
+    using E = MitmEnt<W>;
+    const int nA = N >> 1, nB = N - nA;
+    const int cA = int(binom[nA * BK + g]), cB = int(binom[nB * BK + g]);
+    const int dA = mitm_off(binom, BK, nA, g), sA = dA - int(binom[nA * BK + g - 1]);
+    const int dB = mitm_off(binom, BK, nB, g), sB = dB - int(binom[nB * BK + g - 1]);
+    if (g == 1) {  // L_0: the empty subset
+        if (int(threadIdx.x) < G) ent[threadIdx.x * stride] = ent[threadIdx.x * stride + blockB] = E::zero();
+        __syncthreads();
+    }
+    for (int j = 0; j < G; j++) {
+        typename E::T *L = ent + j * stride;
+        const uint32_t *rows = s_rows + j * N * 2 * W;
+        for (int e = threadIdx.x; e < cA + cB; e += blockDim.x) {
+            const bool inA = e < cA;
+            const int n = inA ? nA : nB, ee = inA ? e : e - cA;
+            int m = n - 1;
+            while (binom[m * BK + g] > (unsigned long long)ee) m--;
+            const int src = ee - int(binom[m * BK + g]);
+            typename E::T *H = inA ? L : L + blockB;
+            H[(inA ? dA : dB) + ee] = E::x(H[(inA ? sA : sB) + src], E::load_row(rows + (inA ? m : nA + m) * 2 * W));
+        }
+    }
+    __syncthreads();
+}
+
+// The pairs of a level, matrix by matrix and h by h: segment k pairs list y (ny entries at
+// oy) with list x (nx entries at ox, the longer one), pair (y, x) at begin + y * nx + x.
+struct MitmSeg {
+    int oy, ny, ox, nx;
+    int hA;           // size of the A-half subset
+    int x_is_a;       // list x is the A half
+    unsigned begin;   // first pair of the segment within its matrix
+};
+constexpr int kMitmMaxSeg = 16;
+
+// segments of level g (thread 0); returns their count
+__device__ __forceinline__ int mitm_segments(int g, int N, const unsigned long long *binom, int BK, int blockB,
+                                             MitmSeg *seg) {
+    const int nA = N >> 1, nB = N - nA;
+    int k = 0;
+    unsigned at = 0;
+    for (int h = 0; h <= g; h++) {
+        const int cA = int(binom_at(binom, BK, nA, h)), cB = int(binom_at(binom, BK, nB, g - h));
+        if (cA == 0 || cB == 0) continue;
+        const int oA = mitm_off(binom, BK, nA, h), oB = blockB + mitm_off(binom, BK, nB, g - h);
+        const bool xa = cA >= cB;
+        seg[k] = MitmSeg{xa ? oB : oA, xa ? cB : cA, xa ? oA : oB, xa ? cA : cB, h, int(xa), at};
+        at += unsigned(cA) * unsigned(cB);
+        k++;
+    }
+    return k;
+}
+
+// every pair of the level for all G matrices: each warp takes a contiguous run of the flat
+// pair space and its lanes walk it 32 apart, so that a step is one conflict-free shared load,
+// the XORs and a POPC per word; the row change (x past nx) is one predicated reload
+template <int W>
+__device__ __forceinline__ void mitm_scan(int g, int G, int N, const MitmSeg *seg, int nseg, unsigned per,
+                                          const unsigned long long *binom, int BK,
+                                          const typename MitmEnt<W>::T *ent, int stride,
+                                          const unsigned long long *s_syn, int SW, unsigned scale, unsigned &best,
+                                          unsigned &wlim) {
+    using E = MitmEnt<W>;
+    const int nA = N >> 1, nB = N - nA;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const unsigned total = unsigned(G) * per;
+    const unsigned per_warp = (((total + nwarps - 1) / nwarps) + 31u) & ~31u;
+    unsigned p = unsigned(warp) * per_warp + lane;
+    const unsigned pend = min(total, unsigned(warp + 1) * per_warp);
+    if (p >= pend) return;
+    int j = int(p / per);
+    unsigned r = p - unsigned(j) * per;
+    int k = 0;
+    while (k + 1 < nseg && seg[k + 1].begin <= r) k++;
+    MitmSeg s = seg[k];
+    r -= s.begin;
+    int y = int(r / unsigned(s.nx)), x = int(r - unsigned(y) * unsigned(s.nx));
+    const typename E::T *L = ent + j * stride;
+    typename E::T a = L[s.oy + y];
+    for (;;) {
+        const unsigned w = E::weight(a, L[s.ox + x]);
+        if (w < wlim) {
+            bool ok = SW == 0;
+            if (!ok) {
+                const int ia = s.x_is_a ? x : y, ib = s.x_is_a ? y : x;
+                const unsigned long long *syn = s_syn + j * N * SW;
+                ok = (mitm_syndrome(binom, BK, nA, s.hA, ia, syn) ^
+                      mitm_syndrome(binom, BK, nB, g - s.hA, ib, syn + nA)) != 0ull;
+            }
+            if (ok) {
+                best = scale * w;
+                wlim = w;
+            }
+        }
+        p += 32;
+        if (p >= pend) break;
+        x += 32;
+        if (x >= s.nx) {
+            do {
+                x -= s.nx;
+                if (++y >= s.ny) {
+                    y = 0;
+                    if (++k == nseg) {
+                        k = 0;
+                        j++;
+                        L = ent + j * stride;
+                    }
+                    s = seg[k];
+                }
+            } while (x >= s.nx);
+            a = L[s.oy + y];
+        }
+    }
+}
+
+// Each thread takes one contiguous lex-rank segment of the level. The lex order varies the
+// last element fastest, so the hot loop is one row XOR onto the (g-1)-prefix accumulator and
+// one POPC per word; the prefix advances (through the local element array) once per run of
+// last elements. The admissibility syndrome is rebuilt only for candidates below the best.
 template <int W>
 __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int code = blockIdx.x;
     const int rowlen = 2 * W;
-    const int G = b.G, N = b.N;
-    const int nrow_words = G * N * rowlen;
-    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem);
-    unsigned long long *s_binom =
-        reinterpret_cast<unsigned long long *>(smem + ((nrow_words * 4 + 15) & ~15));
-    const int nbinom = (N + 1) * b.BK;
-    unsigned long long *s_syn = s_binom + nbinom;
-    const int nsyn = G * N * b.SW;
+    const int N = b.N;
     __shared__ unsigned int s_wmin;
     __shared__ int s_done;
+    __shared__ MitmSeg s_seg[kMitmMaxSeg];
+    __shared__ int s_nseg;
     if (b.in_status && b.in_status[code] != 0) {
         if (threadIdx.x == 0) {
             b.out_upper[code] = b.sentinel;
@@ -390,14 +560,36 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
         }
         return;
     }
+    // matrices of this code: its own count from the device prep, else the batch-wide G
+    const int G = b.n_gammas ? b.n_gammas[code] : b.G;
+    if (G > b.G) {  // more matrices than slots: the host redoes this code with host prep
+        if (threadIdx.x == 0) {
+            b.out_upper[code] = b.sentinel;
+            b.out_generations[code] = 0;
+            b.out_status[code] = kBatchNeedsHostPrep;
+        }
+        return;
+    }
+    const int nrow_words = b.G * N * rowlen;
+    uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem);
+    unsigned long long *s_binom =
+        reinterpret_cast<unsigned long long *>(smem + ((nrow_words * 4 + 15) & ~15));
+    const int nbinom = (N + 1) * b.BK;
+    unsigned long long *s_syn = s_binom + nbinom;
+    // 16-byte aligned offset into the dynamic shared block (pointer arithmetic on smem keeps
+    // the shared address space visible to the compiler)
+    unsigned char *s_mitm =
+        smem + ((reinterpret_cast<unsigned char *>(s_syn + b.G * N * b.SW) - smem + 15) & ~ptrdiff_t(15));
     const uint32_t *grow = b.rows + (size_t)code * b.Gs * N * rowlen;
     const unsigned long long *gsyn = b.syn + (size_t)code * b.Gs * N * b.SW;
-    for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = grow[i];
+    for (int i = threadIdx.x; i < G * N * rowlen; i += blockDim.x) s_rows[i] = grow[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = b.binom[i];
-    for (int i = threadIdx.x; i < nsyn; i += blockDim.x) s_syn[i] = gsyn[i];
+    for (int i = threadIdx.x; i < G * N * b.SW; i += blockDim.x) s_syn[i] = gsyn[i];
     if (threadIdx.x == 0) { s_wmin = unsigned(b.sentinel); s_done = 0; }
     __syncthreads();
 
+    const int SW = b.SW;
+    const unsigned scale = unsigned(b.scale);
     int U = b.sentinel;
     int gen = 0;
     int c[kMaxLevel];
@@ -409,36 +601,71 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
         const unsigned long long total = per * G;
         const unsigned long long seg_len = max(1ull, (total + blockDim.x - 1) / blockDim.x);
         const unsigned long long segs_per = (per + seg_len - 1) / seg_len;
-        // thread-local minimum of the admissible candidates below U; one shared atomic per
-        // warp at the end instead of one per improving candidate
+        // thread-local minimum of the admissible candidates below U (engine units); one shared
+        // atomic per warp at the end instead of one per improving candidate
         unsigned best = unsigned(U);
-        for (unsigned long long seg = threadIdx.x; seg < segs_per * G; seg += blockDim.x) {
+        unsigned wlim = (best + scale - 1) / scale;  // popc < wlim  <=>  scale * popc < best
+        // levels whose half-lists fit stay resident and grow by one size per level
+        const bool mitm = W <= 2 && g <= b.mitm_g && G <= kMitmSlots;
+        if constexpr (W <= 2) {
+            if (mitm) {
+                using T = typename MitmEnt<W>::T;
+                T *ent = reinterpret_cast<T *>(s_mitm);
+                // per matrix: A's lists L_0..L_mitm_g, then B's
+                const int blockB = mitm_off(s_binom, b.BK, N >> 1, b.mitm_g + 1);
+                const int stride = blockB + mitm_off(s_binom, b.BK, N - (N >> 1), b.mitm_g + 1);
+                if (threadIdx.x == 0) s_nseg = mitm_segments(g, N, s_binom, b.BK, blockB, s_seg);
+                mitm_build<W>(g, G, N, s_rows, s_binom, b.BK, ent, blockB, stride);  // ends in a barrier
+                mitm_scan<W>(g, G, N, s_seg, s_nseg, unsigned(per), s_binom, b.BK, ent, stride, s_syn, SW, scale,
+                             best, wlim);
+            }
+        }
+        for (unsigned long long seg = threadIdx.x; seg < (mitm ? 0ull : segs_per * G); seg += blockDim.x) {
             const int j = int(seg / segs_per);
             const unsigned long long r0 = (seg % segs_per) * seg_len;
-            const unsigned long long r1 = min(r0 + seg_len, per);
             const uint32_t *rows = s_rows + j * N * rowlen;
-            const unsigned long long *syn = s_syn + j * N * b.SW;
+            const unsigned long long *syn = s_syn + j * N * SW;
             unrank_lex(r0, g, N, s_binom, b.BK, c);
-            uint32_t acc[2 * W];
+            uint32_t pre[2 * W];
 #pragma unroll
-            for (int i = 0; i < 2 * W; i++) acc[i] = 0;
-            for (int i = 0; i < g; i++) xor_row<W>(acc, rows + c[i] * rowlen);
-            unsigned long long r = r0;
+            for (int i = 0; i < 2 * W; i++) pre[i] = 0;
+            for (int i = 0; i < g - 1; i++) xor_row<W>(pre, rows + c[i] * rowlen);
+            int m = c[g - 1];
+            unsigned long long left = min(r0 + seg_len, per) - r0;
             for (;;) {
-                const unsigned int w = unsigned(b.scale * weight_of<W>(acc));
-                if (w < best && admissible_combo(syn, b.SW, c, g)) best = w;
-                if (++r >= r1) break;
-                int i = g - 1;
+                const int lim = int(min((unsigned long long)N, (unsigned long long)m + left));
+                left -= (unsigned long long)(lim - m);
+                const uint32_t *row = rows + m * rowlen;
+                for (; m < lim; m++, row += rowlen) {
+                    unsigned w = 0;
+#pragma unroll
+                    for (int i = 0; i < W; i++) w += __popc((pre[i] ^ row[i]) | (pre[W + i] ^ row[W + i]));
+                    if (w < wlim) {
+                        bool ok = SW == 0;
+                        for (int s = 0; s < SW && !ok; s++) {
+                            unsigned long long x = syn[m * SW + s];
+                            for (int i = 0; i < g - 1; i++) x ^= syn[c[i] * SW + s];
+                            ok = x != 0;
+                        }
+                        if (ok) {
+                            best = scale * w;
+                            wlim = w;
+                        }
+                    }
+                }
+                if (left == 0 || g == 1) break;
+                // next (g-1)-prefix in lex order; its last element restarts right after it
+                int i = g - 2;
                 while (c[i] == N - g + i) i--;
-                for (int m = i; m < g; m++) xor_row<W>(acc, rows + c[m] * rowlen);
+                for (int q = i; q < g - 1; q++) xor_row<W>(pre, rows + c[q] * rowlen);
                 c[i]++;
-                for (int m = i + 1; m < g; m++) c[m] = c[m - 1] + 1;
-                for (int m = i; m < g; m++) xor_row<W>(acc, rows + c[m] * rowlen);
+                for (int q = i + 1; q < g - 1; q++) c[q] = c[q - 1] + 1;
+                for (int q = i; q < g - 1; q++) xor_row<W>(pre, rows + c[q] * rowlen);
+                m = c[g - 2] + 1;
             }
         }
         for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_down_sync(0xffffffffu, best, o));
         if ((threadIdx.x & 31) == 0 && best < unsigned(U)) atomicMin(&s_wmin, best);
-        (void)total;
         __syncthreads();
         if (threadIdx.x == 0) {
             if (int(s_wmin) < U) U = int(s_wmin);
@@ -1116,11 +1343,42 @@ int launch_walk_impl(const ProblemDev &p, const LevelLaunch &L, cudaStream_t st,
     return 1;
 }
 
+// deepest level whose meet-in-the-middle lists fit kMitmBytes, and their entry count
+constexpr size_t kMitmBytes = 28 * 1024;
+static void mitm_plan(int N, int W, int SW, int BK, int &g_out, int &cap_out) {
+    g_out = 0;
+    cap_out = 0;
+    if (W > 2 || SW > 1 || N < 2) return;
+    const size_t ent = size_t(8 * W) * kMitmSlots;  // x|z sums; syndromes are rebuilt when needed
+    auto C = [](int n, int k) {
+        if (k < 0 || k > n) return 0.0;
+        double c = 1;
+        for (int i = 1; i <= k; i++) c = c * (n - k + i) / i;
+        return c;
+    };
+    const int nA = N / 2, nB = N - nA;
+    double e = 2;  // L_0 of both halves
+    for (int g = 1; g <= N && g + 1 < BK && g < kMitmMaxSeg; g++) {
+        if (C(N, g) * kMitmSlots > 2e9) break;
+        e += C(nA, g) + C(nB, g);
+        if (e * double(ent) > double(kMitmBytes)) break;
+        g_out = g;
+        cap_out = int(e) * kMitmSlots;
+    }
+}
+
 template <int W>
-int launch_batch_impl(const BatchDev &b, cudaStream_t st) {
-    const size_t smem = problem_smem(b.G, b.N, W, b.SW, b.BK);
+int launch_batch_impl(const BatchDev &b_in, cudaStream_t st) {
+    BatchDev b = b_in;
+    mitm_plan(b.N, W, b.SW, b.BK, b.mitm_g, b.mitm_cap);
+    if (b.no_mitm) b.mitm_g = 0;
+    const size_t smem = problem_smem(b.G, b.N, W, b.SW, b.BK) +
+                        (b.mitm_g > 0 ? size_t(b.mitm_cap) * size_t(8 * W) + 16 : 0);
     allow_big_smem<batch_kernel<W>>();
-    batch_kernel<W><<<b.codes, 256, smem, st>>>(b);
+    // one code per CTA; small CTAs when there are many codes, so that every SM holds enough of
+    // them to cover the per-code level barriers (codes finish at different levels)
+    const int threads = b.threads > 0 ? b.threads : 256;
+    batch_kernel<W><<<b.codes, threads, smem, st>>>(b);
     return 1;
 }
 

@@ -19,18 +19,36 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// image rows: 3n <= 192 columns -> 3 words; normalizer rows: 2n <= 128 -> 2 words
+// word i of a register array without dynamic indexing (which would put the array in local
+// memory)
 template <int NW>
-struct WarpRows {
-    unsigned long long v[2][NW];  // rows lane and lane + 32
+__device__ __forceinline__ unsigned long long word_at(const unsigned long long (&w)[NW], int i) {
+    unsigned long long x = w[0];
+#pragma unroll
+    for (int k = 1; k < NW; k++)
+        if (i == k) x = w[k];
+    return x;
+}
 
-    __device__ __forceinline__ bool bit(int slot, int c) const { return (v[slot][c >> 6] >> (c & 63)) & 1ull; }
+template <int NW>
+__device__ __forceinline__ void or_at(unsigned long long (&w)[NW], int i, unsigned long long v) {
+#pragma unroll
+    for (int k = 0; k < NW; k++)
+        if (i == k) w[k] |= v;
+}
+
+// image rows: 3n <= 192 columns -> 3 words; normalizer rows: 2n <= 128 -> 2 words
+template <int S, int NW>
+struct WarpRows {
+    unsigned long long v[2][NW];  // rows lane and lane + 32 (slot 1 only when S == 2)
+
+    __device__ __forceinline__ bool bit(int slot, int c) const { return (word_at(v[slot], c >> 6) >> (c & 63)) & 1ull; }
 
     // row i broadcast to every lane (i warp-uniform)
     __device__ __forceinline__ void fetch(int i, unsigned long long (&out)[NW]) const {
         const int slot = i >> 5, src = i & 31;
 #pragma unroll
-        for (int w = 0; w < NW; w++) out[w] = __shfl_sync(kFull, slot ? v[1][w] : v[0][w], src);
+        for (int w = 0; w < NW; w++) out[w] = __shfl_sync(kFull, (S == 2 && slot) ? v[1][w] : v[0][w], src);
     }
 
     // one step of the reference's elimination (bitvec.cpp:213-233 / prep.cpp:330-346): the
@@ -39,7 +57,7 @@ struct WarpRows {
     __device__ __forceinline__ bool pivot(int c, int r, int rows) {
         const int lane = threadIdx.x & 31;
         const unsigned b0 = __ballot_sync(kFull, lane < rows && lane >= r && bit(0, c));
-        const unsigned b1 = __ballot_sync(kFull, lane + 32 < rows && lane + 32 >= r && bit(1, c));
+        const unsigned b1 = S == 2 ? __ballot_sync(kFull, lane + 32 < rows && lane + 32 >= r && bit(1, c)) : 0u;
         if (!(b0 | b1)) return false;
         const int sel = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
         unsigned long long prow[NW], rrow[NW];
@@ -47,7 +65,7 @@ struct WarpRows {
         fetch(r, rrow);
         if (sel != r) {
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < S; s++) {
                 const int i = lane + 32 * s;
                 if (i == r)
 #pragma unroll
@@ -58,7 +76,7 @@ struct WarpRows {
             }
         }
 #pragma unroll
-        for (int s = 0; s < 2; s++) {
+        for (int s = 0; s < S; s++) {
             const int i = lane + 32 * s;
             if (i < rows && i != r && bit(s, c))
 #pragma unroll
@@ -83,6 +101,7 @@ __device__ __forceinline__ unsigned long long bits_at(const unsigned long long (
     return len == 64 ? x : (x & ((1ull << len) - 1));
 }
 
+template <int S>
 __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
     const int lane = threadIdx.x & 31;
     const int code = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -92,9 +111,9 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
     unsigned char *piv = s_piv[threadIdx.x >> 5];
 
     // ---- load the normalizer (a|b): row i of this code
-    WarpRows<2> A;
+    WarpRows<S, 2> A;
 #pragma unroll
-    for (int s = 0; s < 2; s++) {
+    for (int s = 0; s < S; s++) {
         const int i = lane + 32 * s;
 #pragma unroll
         for (int w = 0; w < 2; w++)
@@ -102,7 +121,7 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
     }
     // mask padding bits beyond 2n
 #pragma unroll
-    for (int s = 0; s < 2; s++)
+    for (int s = 0; s < S; s++)
 #pragma unroll
         for (int w = 0; w < 2; w++) {
             const int lo = 64 * w, hi = min(2 * n, 64 * w + 64);
@@ -113,7 +132,7 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
 
     // ---- validate_normalizer (distance.cpp:71-93); shape checks are done on the host
     if (d.validate) {
-        WarpRows<2> E = A;  // echelon form of A (rank, in_rowspace)
+        WarpRows<S, 2> E = A;  // echelon form of A (rank, in_rowspace)
         int r = 0;
         for (int c = 0; c < 2 * n && r < N; c++)
             if (E.pivot(c, r, N)) piv[r++] = (unsigned char)c;
@@ -122,9 +141,9 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
             status = 2;
         } else {
             // symplectic dual = Euclidean kernel of the half-swapped rows (bitvec.cpp:261-274)
-            WarpRows<2> S;
+            WarpRows<S, 2> Sd;
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < S; s++) {
                 const unsigned long long a = bits_at(A.v[s], 0, n), b = bits_at(A.v[s], n, n);
                 // (b | a) packed at columns [0, n) and [n, 2n)
                 unsigned long long lo = b, hi = 0;
@@ -134,14 +153,14 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
                 } else {
                     hi = a;
                 }
-                S.v[s][0] = lo;
-                S.v[s][1] = 2 * n > 64 ? hi : 0;
+                Sd.v[s][0] = lo;
+                Sd.v[s][1] = 2 * n > 64 ? hi : 0;
             }
             __shared__ unsigned char s_spiv[4][2 * kPrepMaxN];
             unsigned char *spiv = s_spiv[threadIdx.x >> 5];
             int rs = 0;
             for (int c = 0; c < 2 * n && rs < N; c++)
-                if (S.pivot(c, rs, N)) spiv[rs++] = (unsigned char)c;
+                if (Sd.pivot(c, rs, N)) spiv[rs++] = (unsigned char)c;
             // free columns in ascending order; dual vector f: e_f + sum_r S[r][f] e_{spiv[r]}
             // two free columns per lane (n - k <= 64)
             unsigned long long dv[2][2] = {{0, 0}, {0, 0}};
@@ -150,20 +169,23 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
                 int nf = 0, pi = 0;
                 for (int c = 0; c < 2 * n; c++) {
                     if (pi < rs && spiv[pi] == c) { pi++; continue; }
-                    if ((nf & 31) == lane) fcol[nf >> 5] = c;
+                    if ((nf & 31) == lane) {
+                        if (nf >> 5) fcol[1] = c;
+                        else fcol[0] = c;
+                    }
                     nf++;
                 }
             }
 #pragma unroll
-            for (int s = 0; s < 2; s++)
-                if (fcol[s] >= 0) dv[s][fcol[s] >> 6] |= 1ull << (fcol[s] & 63);
+            for (int s = 0; s < S; s++)
+                if (fcol[s] >= 0) or_at(dv[s], fcol[s] >> 6, 1ull << (fcol[s] & 63));
             for (int q = 0; q < rs; q++) {
                 unsigned long long row[2];
-                S.fetch(q, row);
+                Sd.fetch(q, row);
 #pragma unroll
-                for (int s = 0; s < 2; s++)
-                    if (fcol[s] >= 0 && ((row[fcol[s] >> 6] >> (fcol[s] & 63)) & 1ull))
-                        dv[s][spiv[q] >> 6] |= 1ull << (spiv[q] & 63);
+                for (int s = 0; s < S; s++)
+                    if (fcol[s] >= 0 && ((word_at(row, fcol[s] >> 6) >> (fcol[s] & 63)) & 1ull))
+                        or_at(dv[s], spiv[q] >> 6, 1ull << (spiv[q] & 63));
             }
             // in_rowspace(A, v): reduce by the echelon rows of A
             for (int q = 0; q < rankA; q++) {
@@ -171,8 +193,8 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
                 E.fetch(q, row);
                 const int pc = piv[q];
 #pragma unroll
-                for (int s = 0; s < 2; s++)
-                    if ((dv[s][pc >> 6] >> (pc & 63)) & 1ull) {
+                for (int s = 0; s < S; s++)
+                    if ((word_at(dv[s], pc >> 6) >> (pc & 63)) & 1ull) {
                         dv[s][0] ^= row[0];
                         dv[s][1] ^= row[1];
                     }
@@ -183,9 +205,9 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
     }
 
     // ---- isometry_transform: (a | b | a^b) in 3n <= 192 columns
-    WarpRows<3> cur;
+    WarpRows<S, 3> cur;
 #pragma unroll
-    for (int s = 0; s < 2; s++) {
+    for (int s = 0; s < S; s++) {
         const unsigned long long a = bits_at(A.v[s], 0, n), b = bits_at(A.v[s], n, n), c = a ^ b;
         unsigned long long out[3] = {0, 0, 0};
         // place a at 0, b at n, c at 2n
@@ -211,7 +233,7 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
     for (; status == 0;) {
         int r = 0;
         for (int c = 0; c < 3 * n && r < N; c++) {
-            if ((used[c >> 6] >> (c & 63)) & 1ull) continue;
+            if ((word_at(used, c >> 6) >> (c & 63)) & 1ull) continue;
             if (cur.pivot(c, r, N)) piv[r++] = (unsigned char)c;
         }
         if (r == 0) break;
@@ -222,7 +244,7 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
         if (G < d.Gs) {
             // rows of Gamma_G: x = columns [0, n), z = columns [n, 2n) of the image
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < S; s++) {
                 const unsigned long long x = bits_at(cur.v[s], 0, n), z = bits_at(cur.v[s], n, n);
 #pragma unroll
                 for (int j = 0; j < kPrepGammaSlots; j++)
@@ -240,7 +262,7 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
             }
             if (lane == 0) d.deficits[(size_t)code * d.Gs + G] = N - r;
         }
-        for (int q = 0; q < r; q++) used[piv[q] >> 6] |= 1ull << (piv[q] & 63);
+        for (int q = 0; q < r; q++) or_at(used, piv[q] >> 6, 1ull << (piv[q] & 63));
         G++;
     }
 
@@ -257,14 +279,14 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
 #pragma unroll
             for (int j = 0; j < kPrepGammaSlots; j++)
 #pragma unroll
-                for (int s = 0; s < 2; s++)
+                for (int s = 0; s < S; s++)
                     syn[j][s] |= (unsigned long long)((__popcll(gx[j][s] & fb) + __popcll(gz[j][s] & fa)) & 1) << f;
         }
         const int gs = min(G, d.Gs);
 #pragma unroll
         for (int j = 0; j < kPrepGammaSlots; j++)
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < S; s++) {
                 const int i = lane + 32 * s;
                 if (j < gs && i < N) d.syn[((size_t)code * d.Gs + j) * N + i] = syn[j][s];
             }
@@ -292,7 +314,12 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
 int launch_batch_prep(const BatchPrepDev &d, void *stream) {
     if (d.codes <= 0) return 0;
     const int warps = 4;
-    batch_prep_kernel<<<(d.codes + warps - 1) / warps, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
+    const unsigned grid = unsigned((d.codes + warps - 1) / warps);
+    // one row per lane when the normalizer has at most 32 rows, else two
+    if (d.N <= 32)
+        batch_prep_kernel<1><<<grid, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
+    else
+        batch_prep_kernel<2><<<grid, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
     return 1;
 }
 

@@ -226,6 +226,20 @@ def test_batch_device_prep_rejects_what_the_host_rejects(gpu):
     assert st[3] == 2 and st[4] == 2 and (np.delete(st, [3, 4]) == 0).all()
 
 
+@pytest.mark.parametrize("nk", [(20, 2), (12, 3), (30, 4), (40, 6), (33, 31), (3, 1)])
+def test_batch_meet_in_the_middle_matches_walk(gpu, nk):
+    # default: levels whose half-lists fit in shared memory pair A_h x B_(g-h); kernel=1 runs
+    # every level on the per-thread lexicographic walk
+    n, k = nk
+    codes = [gpu.generate_code(n, k, s) for s in range(200, 200 + (256 if n <= 20 else 16))]
+    o = dict(max_generation=4) if n > 30 else {}
+    mitm = gpu.saved_isometry_batch(codes, gpu.RunOptions(**o))
+    walk = gpu.saved_isometry_batch(codes, gpu.RunOptions(kernel=1, **o))
+    assert (mitm.statuses == walk.statuses).all()
+    assert (mitm.distances == walk.distances).all()
+    assert mitm.traces == walk.traces
+
+
 @pytest.mark.parametrize("nk", [(30, 4), (40, 6), (64, 0), (33, 31), (62, 2)])
 def test_batch_device_prep_shapes(gpu, nk):
     # multi-word rows (n > 32), k = 0 (filter off), n + k = 64 rows (two rows per lane)
