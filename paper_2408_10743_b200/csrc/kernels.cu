@@ -15,6 +15,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "device.hpp"
 
@@ -368,33 +370,34 @@ __global__ void __launch_bounds__(256) brute_kernel(BruteDev b) {
 // ---------------------------------------------------------------- batch: one code per CTA
 
 // Meet-in-the-middle levels of the batch kernel. The rows of one matrix split into halves
-// A = [0, nA) and B = [nA, N); list L_h of a half holds the XOR sums (and syndromes) of its
-// h-subsets in colex order, so the g-combinations are exactly the pairs A_h x B_(g-h),
-// h = 0..g. A warp fixes one entry of the shorter list and its lanes stride the longer one:
-// every candidate is one shared load, the XORs and a POPC per word, with no divergence.
+// A = [0, nA) and B = [nA, N); list L_h of a half holds the XOR sums and the admissibility
+// syndromes of its h-subsets in colex order, so the g-combinations are exactly the pairs
+// A_h x B_(g-h), h = 0..g. The lists stay resident from level to level (level g adds L_g).
+// Pairs with an empty side (h = 0 or h = g) are the new L_g entries themselves: they are
+// scored while L_g is built, and the deepest level scores its L_g without storing it.
 template <int W>
 struct MitmEnt;
 template <>
 struct MitmEnt<1> {
     using T = uint2;
-    static __device__ __forceinline__ T zero() { return make_uint2(0u, 0u); }
     static __device__ __forceinline__ T load_row(const uint32_t *r) { return make_uint2(r[0], r[1]); }
     static __device__ __forceinline__ T x(T a, T b) { return make_uint2(a.x ^ b.x, a.y ^ b.y); }
+    static __device__ __forceinline__ unsigned weight(T a) { return __popc(a.x | a.y); }
     static __device__ __forceinline__ unsigned weight(T a, T b) { return __popc((a.x ^ b.x) | (a.y ^ b.y)); }
 };
 template <>
 struct MitmEnt<2> {
     using T = uint4;  // (x0, x1, z0, z1)
-    static __device__ __forceinline__ T zero() { return make_uint4(0u, 0u, 0u, 0u); }
     static __device__ __forceinline__ T load_row(const uint32_t *r) { return make_uint4(r[0], r[1], r[2], r[3]); }
     static __device__ __forceinline__ T x(T a, T b) { return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w); }
+    static __device__ __forceinline__ unsigned weight(T a) { return __popc(a.x | a.z) + __popc(a.y | a.w); }
     static __device__ __forceinline__ unsigned weight(T a, T b) {
         return __popc((a.x ^ b.x) | (a.z ^ b.z)) + __popc((a.y ^ b.y) | (a.w ^ b.w));
     }
 };
 
-// matrices whose lists stay resident (the per-matrix stride is sized for this many)
-constexpr int kMitmSlots = 3;
+// matrices whose lists stay resident: the device prep's slots
+constexpr int kMitmSlots = kPrepGammaSlots;
 
 // first entry of L_h in an n-element half: sum of C(n, s), s < h
 __device__ __forceinline__ int mitm_off(const unsigned long long *binom, int BK, int n, int h) {
@@ -403,137 +406,123 @@ __device__ __forceinline__ int mitm_off(const unsigned long long *binom, int BK,
     return e;
 }
 
-// colex unrank of entry e of L_h of a half into the XOR of the syndromes of its elements
-__device__ __forceinline__ unsigned long long mitm_syndrome(const unsigned long long *binom, int BK, int n, int h,
-                                                            int e, const unsigned long long *syn) {
-    unsigned long long x = 0;
-    int m = n - 1;
-    for (int i = h; i >= 1; i--) {
-        while (binom[m * BK + i] > (unsigned long long)e) m--;
-        x ^= syn[m];
-        e -= int(binom[m * BK + i]);
-        m--;
+// where the lists of one matrix live: A's L_0..L_(stored-1), then B's
+constexpr int kMitmMaxLevel = 15;
+struct MitmView {
+    int nA, nB;
+    int stored;   // lists L_0 .. L_(stored-1) are resident (stored = mitm_g: L_mitm_g never is)
+    int blockB;   // first entry of B's lists
+    int stride;   // entries per matrix
+    const int *cnt;  // [2][kMitmMaxLevel + 1]: C(n_half, h)
+    const int *off;  // [2][kMitmMaxLevel + 1]: first entry of L_h (B's include blockB)
+};
+
+__device__ __forceinline__ void mitm_candidate(unsigned w, unsigned long long syn, int SW, unsigned scale,
+                                               unsigned &best, unsigned &wlim) {
+    if (w < wlim && (SW == 0 || syn != 0ull)) {
+        best = scale * w;
+        wlim = w;
     }
-    return x;
 }
 
-// L_g of both halves of every matrix (and L_0 at g = 1), from the resident L_(g-1):
-// in colex order the g-subsets with maximum m follow those with maximum < m, and their first
-// g - 1 elements are the first C(m, g-1) entries of L_(g-1)
+// L_g of both halves of every matrix from the resident L_(g-1), each entry scored as a
+// candidate on its own (its pair with the other half's empty subset), and stored when a
+// deeper level will read it. In colex order the g-subsets with maximum m come after those
+// with maximum < m, and their first g - 1 elements are the first C(m, g-1) entries of L_(g-1).
 template <int W>
-__device__ __forceinline__ void mitm_build(int g, int G, int N, const uint32_t *s_rows, const unsigned long long *binom,
-                                           int BK, typename MitmEnt<W>::T *ent, int blockB, int stride) {
+__device__ __forceinline__ void mitm_build(int g, int G, int N, const uint32_t *s_rows, const unsigned long long *s_syn,
+                                           int SW, const unsigned long long *binom, int BK, const MitmView &v,
+                                           typename MitmEnt<W>::T *ent, unsigned long long *esyn, unsigned scale,
+                                           unsigned &best, unsigned &wlim) {
     using E = MitmEnt<W>;
-    const int nA = N >> 1, nB = N - nA;
-    const int cA = int(binom[nA * BK + g]), cB = int(binom[nB * BK + g]);
-    const int dA = mitm_off(binom, BK, nA, g), sA = dA - int(binom[nA * BK + g - 1]);
-    const int dB = mitm_off(binom, BK, nB, g), sB = dB - int(binom[nB * BK + g - 1]);
-    if (g == 1) {  // L_0: the empty subset
-        if (int(threadIdx.x) < G) ent[threadIdx.x * stride] = ent[threadIdx.x * stride + blockB] = E::zero();
-        __syncthreads();
-    }
+    const bool store = g < v.stored;
+    constexpr int K = kMitmMaxLevel + 1;
     for (int j = 0; j < G; j++) {
-        typename E::T *L = ent + j * stride;
+        typename E::T *L = ent + j * v.stride;
+        unsigned long long *S = esyn + j * v.stride;
         const uint32_t *rows = s_rows + j * N * 2 * W;
-        for (int e = threadIdx.x; e < cA + cB; e += blockDim.x) {
-            const bool inA = e < cA;
-            const int n = inA ? nA : nB, ee = inA ? e : e - cA;
-            int m = n - 1;
-            while (binom[m * BK + g] > (unsigned long long)ee) m--;
-            const int src = ee - int(binom[m * BK + g]);
-            typename E::T *H = inA ? L : L + blockB;
-            H[(inA ? dA : dB) + ee] = E::x(H[(inA ? sA : sB) + src], E::load_row(rows + (inA ? m : nA + m) * 2 * W));
+        const unsigned long long *syn = s_syn + j * N * SW;
+        for (int half = 0; half < 2; half++) {
+            const int n = half ? v.nB : v.nA, base = half ? v.nA : 0;
+            const int c = v.cnt[half * K + g], dst0 = v.off[half * K + g], src0 = v.off[half * K + g - 1];
+            // entries ascend with the thread's stride, so the maximum m only moves up
+            int m = g - 1;
+            for (int e = threadIdx.x; e < c; e += blockDim.x) {
+                while (binom[(m + 1) * BK + g] <= (unsigned long long)e) m++;
+                const int r = base + m;
+                typename E::T x = E::load_row(rows + r * 2 * W);
+                unsigned long long sy = SW ? syn[r] : 0ull;
+                if (g > 1) {
+                    const int src = src0 + e - int(binom[m * BK + g]);
+                    x = E::x(L[src], x);
+                    if (SW) sy ^= S[src];
+                }
+                mitm_candidate(E::weight(x), sy, SW, scale, best, wlim);
+                if (store) {
+                    L[dst0 + e] = x;
+                    if (SW) S[dst0 + e] = sy;
+                }
+            }
+            (void)n;
         }
     }
     __syncthreads();
 }
 
-// The pairs of a level, matrix by matrix and h by h: segment k pairs list y (ny entries at
-// oy) with list x (nx entries at ox, the longer one), pair (y, x) at begin + y * nx + x.
-struct MitmSeg {
-    int oy, ny, ox, nx;
-    int hA;           // size of the A-half subset
-    int x_is_a;       // list x is the A half
-    unsigned begin;   // first pair of the segment within its matrix
-};
-constexpr int kMitmMaxSeg = 16;
+// the pairs A_h x B_(g-h), 0 < h < g, of one level and all G matrices. A warp takes a block of
+// R rows of the shorter list (round robin over the blocks of every segment, so the warps stay
+// balanced without a barrier) and its lanes stride the longer one: each lane loads one entry
+// per step and scores it against the R rows it holds in registers.
+constexpr int kMitmRows = 4;
 
-// segments of level g (thread 0); returns their count
-__device__ __forceinline__ int mitm_segments(int g, int N, const unsigned long long *binom, int BK, int blockB,
-                                             MitmSeg *seg) {
-    const int nA = N >> 1, nB = N - nA;
-    int k = 0;
-    unsigned at = 0;
-    for (int h = 0; h <= g; h++) {
-        const int cA = int(binom_at(binom, BK, nA, h)), cB = int(binom_at(binom, BK, nB, g - h));
-        if (cA == 0 || cB == 0) continue;
-        const int oA = mitm_off(binom, BK, nA, h), oB = blockB + mitm_off(binom, BK, nB, g - h);
-        const bool xa = cA >= cB;
-        seg[k] = MitmSeg{xa ? oB : oA, xa ? cB : cA, xa ? oA : oB, xa ? cA : cB, h, int(xa), at};
-        at += unsigned(cA) * unsigned(cB);
-        k++;
-    }
-    return k;
-}
-
-// every pair of the level for all G matrices: each warp takes a contiguous run of the flat
-// pair space and its lanes walk it 32 apart, so that a step is one conflict-free shared load,
-// the XORs and a POPC per word; the row change (x past nx) is one predicated reload
-template <int W>
-__device__ __forceinline__ void mitm_scan(int g, int G, int N, const MitmSeg *seg, int nseg, unsigned per,
-                                          const unsigned long long *binom, int BK,
-                                          const typename MitmEnt<W>::T *ent, int stride,
-                                          const unsigned long long *s_syn, int SW, unsigned scale, unsigned &best,
+template <int W, int R>
+__device__ __forceinline__ void mitm_rows(int oy, int ny, int ox, int nx, int yb, const typename MitmEnt<W>::T *L,
+                                          const unsigned long long *S, int SW, unsigned scale, unsigned &best,
                                           unsigned &wlim) {
     using E = MitmEnt<W>;
-    const int nA = N >> 1, nB = N - nA;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const unsigned total = unsigned(G) * per;
-    const unsigned per_warp = (((total + nwarps - 1) / nwarps) + 31u) & ~31u;
-    unsigned p = unsigned(warp) * per_warp + lane;
-    const unsigned pend = min(total, unsigned(warp + 1) * per_warp);
-    if (p >= pend) return;
-    int j = int(p / per);
-    unsigned r = p - unsigned(j) * per;
-    int k = 0;
-    while (k + 1 < nseg && seg[k + 1].begin <= r) k++;
-    MitmSeg s = seg[k];
-    r -= s.begin;
-    int y = int(r / unsigned(s.nx)), x = int(r - unsigned(y) * unsigned(s.nx));
-    const typename E::T *L = ent + j * stride;
-    typename E::T a = L[s.oy + y];
-    for (;;) {
-        const unsigned w = E::weight(a, L[s.ox + x]);
-        if (w < wlim) {
-            bool ok = SW == 0;
-            if (!ok) {
-                const int ia = s.x_is_a ? x : y, ib = s.x_is_a ? y : x;
-                const unsigned long long *syn = s_syn + j * N * SW;
-                ok = (mitm_syndrome(binom, BK, nA, s.hA, ia, syn) ^
-                      mitm_syndrome(binom, BK, nB, g - s.hA, ib, syn + nA)) != 0ull;
-            }
-            if (ok) {
+    typename E::T a[R];
+#pragma unroll
+    for (int i = 0; i < R; i++) a[i] = L[oy + min(yb * R + i, ny - 1)];
+    for (int x = threadIdx.x & 31; x < nx; x += 32) {
+        const typename E::T u = L[ox + x];
+#pragma unroll
+        for (int i = 0; i < R; i++) {
+            const unsigned w = E::weight(a[i], u);
+            if (w < wlim && (SW == 0 || (S[oy + min(yb * R + i, ny - 1)] ^ S[ox + x]) != 0ull)) {
                 best = scale * w;
                 wlim = w;
             }
         }
-        p += 32;
-        if (p >= pend) break;
-        x += 32;
-        if (x >= s.nx) {
-            do {
-                x -= s.nx;
-                if (++y >= s.ny) {
-                    y = 0;
-                    if (++k == nseg) {
-                        k = 0;
-                        j++;
-                        L = ent + j * stride;
-                    }
-                    s = seg[k];
-                }
-            } while (x >= s.nx);
-            a = L[s.oy + y];
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void mitm_scan(int g, int G, const unsigned long long *binom, int BK, const MitmView &v,
+                                          const typename MitmEnt<W>::T *ent, const unsigned long long *esyn, int SW,
+                                          unsigned scale, unsigned &best, unsigned &wlim) {
+    constexpr int R = kMitmRows;
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int t0 = warp;  // block index carried across segments
+    for (int j = 0; j < G; j++) {
+        const typename MitmEnt<W>::T *L = ent + j * v.stride;
+        const unsigned long long *S = esyn + j * v.stride;
+        constexpr int K = kMitmMaxLevel + 1;
+        for (int h = 1; h < g; h++) {
+            const int cA = v.cnt[h], cB = v.cnt[K + g - h];
+            if (cA == 0 || cB == 0) continue;
+            const int oA = v.off[h], oB = v.off[K + g - h];
+            const bool xa = cA >= cB;  // lanes stride the longer list
+            const int oy = xa ? oB : oA, ny = xa ? cB : cA, ox = xa ? oA : oB, nx = xa ? cA : cB;
+            const bool wide = ny >= R;
+            const int blocks = wide ? (ny + R - 1) / R : ny;
+            int t = t0;
+            for (; t < blocks; t += nwarps) {
+                if (wide)
+                    mitm_rows<W, R>(oy, ny, ox, nx, t, L, S, SW, scale, best, wlim);
+                else
+                    mitm_rows<W, 1>(oy, ny, ox, nx, t, L, S, SW, scale, best, wlim);
+            }
+            t0 = t - blocks;
         }
     }
 }
@@ -550,8 +539,6 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     const int N = b.N;
     __shared__ unsigned int s_wmin;
     __shared__ int s_done;
-    __shared__ MitmSeg s_seg[kMitmMaxSeg];
-    __shared__ int s_nseg;
     if (b.in_status && b.in_status[code] != 0) {
         if (threadIdx.x == 0) {
             b.out_upper[code] = b.sentinel;
@@ -585,6 +572,21 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     for (int i = threadIdx.x; i < G * N * rowlen; i += blockDim.x) s_rows[i] = grow[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = b.binom[i];
     for (int i = threadIdx.x; i < G * N * b.SW; i += blockDim.x) s_syn[i] = gsyn[i];
+    // list sizes and offsets of the meet-in-the-middle levels: [half][h]
+    __shared__ int s_mcnt[2 * (kMitmMaxLevel + 1)], s_moff[2 * (kMitmMaxLevel + 1)];
+    if (b.mitm_g > 0 && threadIdx.x < 2) {
+        const int half = threadIdx.x, n = half ? N - (N >> 1) : (N >> 1);
+        int at = half ? mitm_off(b.binom, b.BK, N >> 1, b.mitm_g) : 0;  // s_binom is not loaded yet
+        for (int h = 0; h <= kMitmMaxLevel; h++) {
+            const int c = h <= b.mitm_g ? int(binom_at(b.binom, b.BK, n, h)) : 0;
+            s_mcnt[half * (kMitmMaxLevel + 1) + h] = c;
+            s_moff[half * (kMitmMaxLevel + 1) + h] = at;
+            at += h < b.mitm_g ? c : 0;
+        }
+    }
+    // the rank deficits, read once: the level close below is a serial section of thread 0
+    __shared__ int s_def[kPrepGammaSlots];
+    if (threadIdx.x < kPrepGammaSlots) s_def[threadIdx.x] = int(threadIdx.x) < G ? b.deficits[(size_t)code * b.Gs + threadIdx.x] : 0;
     if (threadIdx.x == 0) { s_wmin = unsigned(b.sentinel); s_done = 0; }
     __syncthreads();
 
@@ -595,12 +597,6 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     int c[kMaxLevel];
     const int g_last = b.max_g > 0 ? min(N, b.max_g) : N;
     for (int g = 1; g <= g_last; g++) {
-        const unsigned long long per = binom_at(s_binom, b.BK, N, g);
-        // one segment per thread: tiny levels get a candidate or two per thread, not a long
-        // serial walk on a few of them
-        const unsigned long long total = per * G;
-        const unsigned long long seg_len = max(1ull, (total + blockDim.x - 1) / blockDim.x);
-        const unsigned long long segs_per = (per + seg_len - 1) / seg_len;
         // thread-local minimum of the admissible candidates below U (engine units); one shared
         // atomic per warp at the end instead of one per improving candidate
         unsigned best = unsigned(U);
@@ -610,17 +606,32 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
         if constexpr (W <= 2) {
             if (mitm) {
                 using T = typename MitmEnt<W>::T;
+                MitmView v;
+                v.nA = N >> 1;
+                v.nB = N - v.nA;
+                v.stored = b.mitm_g;
+                v.blockB = s_moff[v.stored];
+                v.stride = s_moff[kMitmMaxLevel + 1 + v.stored];
+                v.cnt = s_mcnt;
+                v.off = s_moff;
                 T *ent = reinterpret_cast<T *>(s_mitm);
-                // per matrix: A's lists L_0..L_mitm_g, then B's
-                const int blockB = mitm_off(s_binom, b.BK, N >> 1, b.mitm_g + 1);
-                const int stride = blockB + mitm_off(s_binom, b.BK, N - (N >> 1), b.mitm_g + 1);
-                if (threadIdx.x == 0) s_nseg = mitm_segments(g, N, s_binom, b.BK, blockB, s_seg);
-                mitm_build<W>(g, G, N, s_rows, s_binom, b.BK, ent, blockB, stride);  // ends in a barrier
-                mitm_scan<W>(g, G, N, s_seg, s_nseg, unsigned(per), s_binom, b.BK, ent, stride, s_syn, SW, scale,
-                             best, wlim);
+                unsigned long long *esyn = reinterpret_cast<unsigned long long *>(s_mitm + size_t(b.mitm_cap) * sizeof(T));
+#ifndef SDB_EXP_NOBUILD
+                mitm_build<W>(g, G, N, s_rows, s_syn, SW, s_binom, b.BK, v, ent, esyn, scale, best, wlim);
+#else
+                __syncthreads();
+#endif
+#ifndef SDB_EXP_NOSCAN
+                mitm_scan<W>(g, G, s_binom, b.BK, v, ent, esyn, SW, scale, best, wlim);
+#endif
             }
         }
-        for (unsigned long long seg = threadIdx.x; seg < (mitm ? 0ull : segs_per * G); seg += blockDim.x) {
+        // one segment per thread: tiny levels get a candidate or two per thread, not a long
+        // serial walk on a few of them
+        const unsigned long long per = mitm ? 0ull : binom_at(s_binom, b.BK, N, g);
+        const unsigned long long seg_len = mitm ? 1ull : max(1ull, (per * G + blockDim.x - 1) / blockDim.x);
+        const unsigned long long segs_per = mitm ? 0ull : (per + seg_len - 1) / seg_len;
+        for (unsigned long long seg = threadIdx.x; seg < segs_per * G; seg += blockDim.x) {
             const int j = int(seg / segs_per);
             const unsigned long long r0 = (seg % segs_per) * seg_len;
             const uint32_t *rows = s_rows + j * N * rowlen;
@@ -671,7 +682,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
             if (int(s_wmin) < U) U = int(s_wmin);
             long lower = 0;
             for (int j = 0; j < G; j++) {
-                const int t = g + 1 - b.deficits[(size_t)code * b.Gs + j];
+                const int t = g + 1 - (j < kPrepGammaSlots ? s_def[j] : b.deficits[(size_t)code * b.Gs + j]);
                 lower += t > 0 ? t : 0;
             }
             b.out_trace_lower[(size_t)code * N + g - 1] = int(lower);
@@ -1343,13 +1354,14 @@ int launch_walk_impl(const ProblemDev &p, const LevelLaunch &L, cudaStream_t st,
     return 1;
 }
 
-// deepest level whose meet-in-the-middle lists fit kMitmBytes, and their entry count
-constexpr size_t kMitmBytes = 28 * 1024;
+// deepest meet-in-the-middle level: level g reads L_0..L_(g-1) of both halves of every slot,
+// resident in shared memory (x|z sums and syndromes); returns it and the entries per slot set
+constexpr size_t kMitmBytes = 40 * 1024;
 static void mitm_plan(int N, int W, int SW, int BK, int &g_out, int &cap_out) {
     g_out = 0;
     cap_out = 0;
     if (W > 2 || SW > 1 || N < 2) return;
-    const size_t ent = size_t(8 * W) * kMitmSlots;  // x|z sums; syndromes are rebuilt when needed
+    const size_t ent = (size_t(8 * W) + size_t(8 * SW)) * kMitmSlots;
     auto C = [](int n, int k) {
         if (k < 0 || k > n) return 0.0;
         double c = 1;
@@ -1357,10 +1369,9 @@ static void mitm_plan(int N, int W, int SW, int BK, int &g_out, int &cap_out) {
         return c;
     };
     const int nA = N / 2, nB = N - nA;
-    double e = 2;  // L_0 of both halves
-    for (int g = 1; g <= N && g + 1 < BK && g < kMitmMaxSeg; g++) {
-        if (C(N, g) * kMitmSlots > 2e9) break;
-        e += C(nA, g) + C(nB, g);
+    double e = 0;  // entries of L_0..L_(g-1), both halves
+    for (int g = 1; g <= N && g + 1 < BK && g <= kMitmMaxLevel; g++) {
+        e += C(nA, g - 1) + C(nB, g - 1);
         if (e * double(ent) > double(kMitmBytes)) break;
         g_out = g;
         cap_out = int(e) * kMitmSlots;
@@ -1373,11 +1384,14 @@ int launch_batch_impl(const BatchDev &b_in, cudaStream_t st) {
     mitm_plan(b.N, W, b.SW, b.BK, b.mitm_g, b.mitm_cap);
     if (b.no_mitm) b.mitm_g = 0;
     const size_t smem = problem_smem(b.G, b.N, W, b.SW, b.BK) +
-                        (b.mitm_g > 0 ? size_t(b.mitm_cap) * size_t(8 * W) + 16 : 0);
+                        (b.mitm_g > 0 ? size_t(b.mitm_cap) * size_t(8 * W + 8 * b.SW) + 16 : 0);
     allow_big_smem<batch_kernel<W>>();
     // one code per CTA; small CTAs when there are many codes, so that every SM holds enough of
     // them to cover the per-code level barriers (codes finish at different levels)
     const int threads = b.threads > 0 ? b.threads : 256;
+    if (std::getenv("SDB_TRACE_HOST"))
+        std::fprintf(stderr, "[sdb] batch kernel: %d codes x %d threads, %zu B smem, meet-in-the-middle levels <= %d (%d entries)\n",
+                     b.codes, threads, smem, b.mitm_g, b.mitm_cap);
     batch_kernel<W><<<b.codes, threads, smem, st>>>(b);
     return 1;
 }
