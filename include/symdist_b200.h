@@ -104,8 +104,9 @@ typedef struct {
     int world;              /* number of shards (GPUs); 1 = single GPU */
     sdb_allreduce_min_fn allreduce_min;
     void *allreduce_ctx;
-    int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel (batch: every level on
-                               the per-thread walk, no meet-in-the-middle lists), 2 force the tile
+    int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel (batch: row-major device
+                               prep and every level on the per-thread walk, no meet-in-the-middle
+                               lists), 2 force the tile
                                kernel, 3 batch only: run the prep (validation, information sets) on
                                the host */
     void *stream;           /* cudaStream_t to run on (NULL: a private non-blocking stream) */

@@ -268,6 +268,7 @@ struct BatchPrepDev {
     int *n_gammas;                          // [codes]
     int *status;                            // [codes]: 0 ok, 2 validation
     int Gs;
+    int force_rows;                         // 1: the row-major kernel even for small codes (tests)
 };
 int launch_batch_prep(const BatchPrepDev &d, void *stream);
 

@@ -1150,6 +1150,7 @@ static void run_batch_device(const uint64_t *rows, int n_codes, int n_rows, int 
     pd.validate = o.validate;
     pd.filter = SW;
     pd.Gs = Gs;
+    pd.force_rows = o.kernel == 1;
     const auto t1 = clk::now();
     std::memcpy(h_up, rows, in_bytes);
     std::memcpy(h_up + b_in, h_binom.data(), binom_bytes);

@@ -309,14 +309,177 @@ __global__ void __launch_bounds__(128) batch_prep_kernel(BatchPrepDev d) {
     }
 }
 
+// ---- small codes (n + k <= 32 rows, n <= 32): column-major elimination
+//
+// Lane c holds column c of the isometry image (slot s: column 32 s + c) as a 32-bit mask over
+// the rows. A pivot step of information_sets — the first row sel >= r with a 1 in column c
+// becomes row r, then row r is XORed into every other row with a 1 there — is then one shuffle
+// (the pivot column) and a few lane-local bit operations on each held column: swap bits r and
+// sel, and XOR the pivot column (minus bit r) into every column with bit r set. Same rule,
+// same Gamma_j as the row-major kernel above and the host.
+//
+// validate_normalizer's dual test uses rank(A) = N (checked by the first information set) and
+// rank(A Omega A^T) = 2k: the symplectic dual V^perp of the N-dimensional rowspace V lies in V
+// iff dim(V cap V^perp) = N - rank(A Omega A^T) equals dim V^perp = 2n - N.
+__device__ __forceinline__ unsigned swap_bits(unsigned x, int r, int sel) {
+    const unsigned t = ((x >> r) ^ (x >> sel)) & 1u;
+    return x ^ ((t << r) | (t << sel));
+}
+
+__global__ void __launch_bounds__(128) batch_prep_small_kernel(BatchPrepDev d) {
+    const int lane = threadIdx.x & 31;
+    const int code = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (code >= d.codes) return;
+    const int N = d.N, n = d.n;
+    const unsigned nmask = n == 32 ? ~0u : ((1u << n) - 1u);
+
+    // row `lane` of the normalizer: a (columns [0, n)) and b (columns [n, 2n))
+    unsigned a = 0, b = 0;
+    if (lane < N) {
+        const unsigned long long w0 = d.normalizers[((size_t)code * N + lane) * d.in_words];
+        const unsigned long long w1 = d.in_words > 1 ? d.normalizers[((size_t)code * N + lane) * d.in_words + 1] : 0ull;
+        a = unsigned(w0) & nmask;
+        b = unsigned(n == 32 ? w1 : (w0 >> n)) & nmask;
+    }
+    int status = 0;
+
+    if (d.validate) {
+        // Gram row: bit j = <row lane, row j>_s
+        unsigned gram = 0;
+        for (int j = 0; j < N; j++) {
+            const unsigned aj = __shfl_sync(kFull, a, j), bj = __shfl_sync(kFull, b, j);
+            gram |= ((__popc(a & bj) ^ __popc(b & aj)) & 1u) << j;
+        }
+        if (lane >= N) gram = 0;
+        int rank = 0;
+        bool done = false;
+        for (int c = 0; c < N; c++) {
+            const unsigned cand = __ballot_sync(kFull, !done && ((gram >> c) & 1u));
+            if (!cand) continue;
+            const int p = __ffs(cand) - 1;
+            const unsigned prow = __shfl_sync(kFull, gram, p);
+            if (lane == p) done = true;
+            else if ((gram >> c) & 1u) gram ^= prow;
+            rank++;
+        }
+        if (rank != 2 * (N - n)) status = 2;
+    }
+
+    // image columns (a | b | a^b): column c in lane c & 31, slot c >> 5
+    unsigned col[3] = {0u, 0u, 0u};
+    const unsigned ab = a ^ b;
+    for (int c = 0; c < 3 * n; c++) {
+        const int part = c < n ? 0 : (c < 2 * n ? 1 : 2), bit = c - part * n;
+        const unsigned src = part == 0 ? a : (part == 1 ? b : ab);
+        const unsigned v = __ballot_sync(kFull, lane < N && ((src >> bit) & 1u));
+        if (lane == (c & 31)) {
+#pragma unroll
+            for (int s = 0; s < 3; s++)
+                if (s == (c >> 5)) col[s] = v;
+        }
+    }
+
+    // information_sets (prep.cpp:317-364): greedy elimination on unused columns, carried over
+    unsigned used[3] = {0u, 0u, 0u};  // warp-uniform: bit c & 31 of word c >> 5
+    unsigned gx[kPrepGammaSlots], gz[kPrepGammaSlots];
+#pragma unroll
+    for (int j = 0; j < kPrepGammaSlots; j++) gx[j] = gz[j] = 0u;
+    int G = 0;
+    const int rowlen = 2;  // W = 1
+    for (; status == 0;) {
+        int r = 0;
+        unsigned piv[3] = {0u, 0u, 0u};  // pivot columns of this round
+        for (int c = 0; c < 3 * n && r < N; c++) {
+            const int sc = c >> 5, lc = c & 31;
+            unsigned us = used[0], cs = col[0];
+#pragma unroll
+            for (int s = 1; s < 3; s++)
+                if (s == sc) {
+                    us = used[s];
+                    cs = col[s];
+                }
+            if ((us >> lc) & 1u) continue;
+            const unsigned pcol = __shfl_sync(kFull, cs, lc);
+            const unsigned cand = pcol & (~0u << r);
+            if (!cand) continue;
+            const int sel = __ffs(cand) - 1;
+            const unsigned pc = swap_bits(pcol, r, sel), m = pc & ~(1u << r);
+#pragma unroll
+            for (int s = 0; s < 3; s++) {
+                unsigned x = swap_bits(col[s], r, sel);
+                if ((x >> r) & 1u) x ^= m;
+                col[s] = x;
+            }
+#pragma unroll
+            for (int s = 0; s < 3; s++)
+                if (s == sc) piv[s] |= 1u << lc;
+            r++;
+        }
+        if (r == 0) break;
+        if (G == 0 && r != N) {  // information_sets: rows are linearly dependent
+            status = 2;
+            break;
+        }
+        if (G < d.Gs) {
+            // rows of Gamma_G: row i = bit i of every column; x = columns [0, n), z = [n, 2n)
+            unsigned long long lo = 0ull;  // this lane's row, columns [0, 64)
+            for (int i = 0; i < N; i++) {
+                const unsigned w0 = __ballot_sync(kFull, (col[0] >> i) & 1u);
+                const unsigned w1 = __ballot_sync(kFull, (col[1] >> i) & 1u);
+                if (lane == i) lo = (unsigned long long)w0 | ((unsigned long long)w1 << 32);
+            }
+            const unsigned x = unsigned(lo) & nmask, z = unsigned(lo >> n) & nmask;
+#pragma unroll
+            for (int j = 0; j < kPrepGammaSlots; j++)
+                if (j == G) {
+                    gx[j] = x;
+                    gz[j] = z;
+                }
+            if (lane < N) {
+                uint32_t *dst = d.rows + (((size_t)code * d.Gs + G) * N + lane) * rowlen;
+                dst[0] = x;
+                dst[1] = z;
+            }
+            if (lane == 0) d.deficits[(size_t)code * d.Gs + G] = N - r;
+        }
+#pragma unroll
+        for (int s = 0; s < 3; s++) used[s] |= piv[s];
+        G++;
+    }
+
+    // admissibility syndromes: bit f of row i = <first 2n columns of row i, A_f>_s
+    if (status == 0 && d.filter) {
+        unsigned long long syn[kPrepGammaSlots];
+#pragma unroll
+        for (int j = 0; j < kPrepGammaSlots; j++) syn[j] = 0ull;
+        for (int f = 0; f < N; f++) {
+            const unsigned fa = __shfl_sync(kFull, a, f), fb = __shfl_sync(kFull, b, f);
+#pragma unroll
+            for (int j = 0; j < kPrepGammaSlots; j++)
+                syn[j] |= (unsigned long long)((__popc(gx[j] & fb) ^ __popc(gz[j] & fa)) & 1) << f;
+        }
+        const int gs = min(G, d.Gs);
+#pragma unroll
+        for (int j = 0; j < kPrepGammaSlots; j++)
+            if (j < gs && lane < N) d.syn[((size_t)code * d.Gs + j) * N + lane] = syn[j];
+    }
+    if (lane == 0) {
+        d.status[code] = status;
+        d.n_gammas[code] = G;
+    }
+}
+
 }  // namespace
 
 int launch_batch_prep(const BatchPrepDev &d, void *stream) {
     if (d.codes <= 0) return 0;
     const int warps = 4;
     const unsigned grid = unsigned((d.codes + warps - 1) / warps);
-    // one row per lane when the normalizer has at most 32 rows, else two
-    if (d.N <= 32)
+    // column-major elimination when rows and columns fit a lane's word; else one row per lane
+    // (two when the normalizer has more than 32 rows)
+    if (d.N <= 32 && d.n <= 32 && d.W == 1 && !d.force_rows)
+        batch_prep_small_kernel<<<grid, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
+    else if (d.N <= 32)
         batch_prep_kernel<1><<<grid, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
     else
         batch_prep_kernel<2><<<grid, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(d);
