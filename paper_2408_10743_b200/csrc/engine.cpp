@@ -850,7 +850,13 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     if (opts_.max_generation > 0) g_limit = std::min(g_limit, opts_.max_generation);
     if (g_limit > kMaxLevel) g_limit = kMaxLevel;  // checked again below if the run gets there
     constexpr unsigned long long kSyncCandidates = 1ull << 28;  // ~0.1 ms of kernel time
-    int launches = 0, last_g = 0;
+    // levels enqueued past the last check: a level after termination costs its (empty) launches,
+    // so small codes (whose levels are all tiny) check every few levels
+#ifndef SDB_MAX_UNCHECKED_LEVELS
+#define SDB_MAX_UNCHECKED_LEVELS 4
+#endif
+    constexpr int kMaxUncheckedLevels = SDB_MAX_UNCHECKED_LEVELS;
+    int launches = 0, last_g = 0, checked_g = 0;
     unsigned long long h2d = 0, d2h = 0;
     launches += launch_run_init(pd_, unsigned(sentinel_), d_counter_init_, d_counters_, N_ + 1, stream_);
     check_cuda(cudaGetLastError(), "run init launch");
@@ -908,10 +914,12 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         if (level_seconds) check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
         last_g = g;
         const unsigned long long total = level_candidates(g);
-        if ((lv.sharded && !opts_.comm) || total >= kSyncCandidates || g == g_limit) {
+        if ((lv.sharded && !opts_.comm) || total >= kSyncCandidates || g == g_limit ||
+            g - checked_g >= kMaxUncheckedLevels) {
             check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
             check_cuda(cudaStreamSynchronize(stream_), "level sync");
             d2h += sizeof ctl;
+            checked_g = g;
             if (ctl.done) break;
         }
         if (!packaged_ && g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
