@@ -162,17 +162,33 @@ int build_syndromes(const std::vector<GammaIn> &gammas, int n, const Filter &f, 
     const int G = int(gammas.size()), F = f.rows.rows;
     int N = 0;
     for (const GammaIn &gm : gammas) N = std::max(N, gm.matrix.rows);
-    // S: (G*N) x F, bit (i, r) = <first 2n columns of Gamma row i, filter row r>_s
+    // S: (G*N) x F, bit (i, r) = <first 2n columns of Gamma row i, filter row r>_s (the
+    // reference's projection, engine.cpp:168-173), from word-aligned copies of both halves:
+    // <(x|z), (a|b)>_s = parity(popc(x & b) + popc(z & a))
     BitMat S(G * N, F);
-    std::vector<uint64_t> proj(size_t((2 * n + 63) / 64));
+    const int hw = (n + 63) / 64;
+    auto halves = [&](const BitMat &m, int r, uint64_t *x, uint64_t *z) {
+        for (int w = 0; w < hw; w++) {
+            const int len = std::min(64, n - 64 * w);
+            const uint64_t mask = len == 64 ? ~uint64_t(0) : ((uint64_t(1) << len) - 1);
+            x[w] = row_bits64(m, r, 64 * w) & mask;
+            z[w] = row_bits64(m, r, n + 64 * w) & mask;
+        }
+    };
+    std::vector<uint64_t> fa(size_t(F) * size_t(hw)), fb(size_t(F) * size_t(hw)), x(static_cast<size_t>(hw)),
+        z(static_cast<size_t>(hw));
+    for (int r = 0; r < F; r++) halves(f.rows, r, &fa[size_t(r) * hw], &fb[size_t(r) * hw]);
     for (int j = 0; j < G; j++)
         for (int i = 0; i < gammas[size_t(j)].matrix.rows; i++) {
-            // first 2n columns of the row (the reference's projection, engine.cpp:168-173)
-            const uint64_t *src = gammas[size_t(j)].matrix.row(i);
-            for (size_t w = 0; w < proj.size(); w++) proj[w] = src[w];
-            if ((2 * n) & 63) proj.back() &= (uint64_t(1) << ((2 * n) & 63)) - 1;
-            for (int r = 0; r < F; r++)
-                if (symplectic_ip(proj.data(), f.rows.row(r), n)) S.set(j * N + i, r, true);
+            halves(gammas[size_t(j)].matrix, i, x.data(), z.data());
+            uint64_t *dst = S.row(j * N + i);
+            for (int r = 0; r < F; r++) {
+                int p = 0;
+                for (int w = 0; w < hw; w++)
+                    p += __builtin_popcountll(x[size_t(w)] & fb[size_t(r) * hw + w]) +
+                         __builtin_popcountll(z[size_t(w)] & fa[size_t(r) * hw + w]);
+                if (p & 1) dst[r >> 6] |= uint64_t(1) << (r & 63);
+            }
         }
     // every candidate syndrome lies in rowspace(S); it is zero iff it vanishes on the
     // pivot columns of S's echelon form, so keep only those columns
