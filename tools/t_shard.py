@@ -43,11 +43,16 @@ for cid, gmax in ((4, 0), (5, 9)):
     t1 = sum(base.level_seconds)
     n_levels = len(base.level_seconds)
     sentinel = 3 * c["n"] + 1
+    # levels with fewer candidates than shard_min run whole on every rank (no exchange)
+    shard_min = int(os.environ.get("SHARD_MIN", str(1 << 26)))
+    from math import comb
+    N = c["n"] + c["k"]
+    sharded = [g for g in range(1, n_levels + 1) if 3 * comb(N, g) >= shard_min]
     for world in (2, 4, 8):
         per_level = None
         for r in range(world):
-            ga = GlobalAnswer(base.trace_tuples(), sentinel, list(range(1, n_levels + 1)))
-            o = P.RunOptions(rank=r, world=world, allreduce_min=ga, max_generation=gmax, shard_min=1)
+            ga = GlobalAnswer(base.trace_tuples(), sentinel, sharded)
+            o = P.RunOptions(rank=r, world=world, allreduce_min=ga, max_generation=gmax, shard_min=shard_min)
             with P.Plan(a, o) as pl:
                 pl.run()
                 ga.calls = 0
