@@ -582,6 +582,13 @@ cudaEvent_t Plan::level_event(int i) {
 
 size_t tile_smem_bytes(int G, int N, int W, int K, int BK);
 
+// Cost-model constants of choose_tile, fitted to a (t, tchunk) sweep of config 4 levels 6-8
+// and config 2 levels 4-6 (tools/t_tchunk.py, profiles/r01_tchunk_sweep.log): a unit costs
+// about 40k candidate-equivalents of dispensing, staging and head generation, and the last
+// units leave about 0.4 of the biggest one as tail.
+constexpr double kTileUnitCost = 40000;
+constexpr double kTileTailFraction = 0.4;
+
 TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
                        int world) {
     TileChoice best{0, kTailChunk};
@@ -590,8 +597,8 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
     if (forced_kernel != 2 && total < double(1 << 16)) return best;
     // Level time in candidate-equivalents per CTA slot: max(total load / slots, the largest
     // unit) — a level with few big units is bound by its slowest CTA. A tile unit costs its
-    // padded candidates (every lane of a warp with heads runs H heads) plus ~20k for the
-    // dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
+    // padded candidates (every lane of a warp with heads runs H heads) plus kTileUnitCost for
+    // the dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
     // (measured 1.4e11 vs 3.9e12 cand/s) with perfectly fine granularity.
     const double Hl = heads_per_lane(W), HBk = head_block(W);
     const double slots = double(num_sms) * tile_blocks_per_sm(W) * std::max(1, world);  // all ranks' CTAs
@@ -612,15 +619,16 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
                 const double heads_last = Hb - (nH - 1) * HBk;
                 const double warps_full = kTileThreads / 32.0, warps_last = std::ceil(heads_last / (32.0 * Hl));
                 const double tc = Tb / nT;  // average tails per unit
-                const double unit_full = warps_full * 32 * Hl * tc + 20000, unit_last = warps_last * 32 * Hl * tc + 20000;
+                const double unit_full = warps_full * 32 * Hl * tc + kTileUnitCost,
+                             unit_last = warps_last * 32 * Hl * tc + kTileUnitCost;
                 sum += nT * ((nH - 1) * unit_full + unit_last);
                 biggest = std::max(biggest, nH > 1 ? unit_full : unit_last);
             }
             sum *= G;
             // the average load per CTA slot plus the tail: the last units finish unevenly,
-            // about half the biggest unit late on average (this matters when sharding leaves
+            // a fraction of the biggest unit late on average (this matters when sharding leaves
             // few units per CTA)
-            const double time = std::max(sum / slots + 0.5 * biggest, biggest);
+            const double time = std::max(sum / slots + kTileTailFraction * biggest, biggest);
             if (time < best_time) {
                 best_time = time;
                 best = TileChoice{t, tchunk};
@@ -789,7 +797,16 @@ void Plan::prepare_level(int g) {
     const unsigned long long per = binom_u64(N_, g);
     if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
     const unsigned long long total = per * (unsigned long long)G_;
-    const TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_, world);
+    TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_, world);
+    if (const char *force = std::getenv("SDB_TILE_FORCE")) {  // experiments: "g:t:tchunk,..."
+        for (const char *q = force; *q;) {
+            int fg = 0, ft = 0, fc = 0, used = 0;
+            if (std::sscanf(q, "%d:%d:%d%n", &fg, &ft, &fc, &used) != 3) break;
+            if (fg == g && ft >= 0 && ft < g && fc >= 2 && fc <= kTailChunk) tc = TileChoice{ft, fc};
+            q += used;
+            if (*q == ',') q++;
+        }
+    }
     lv.t = tc.t;
     if (lv.t == 0) {
         LevelLaunch &LL = lv.walk;
