@@ -210,6 +210,26 @@ sdb_status sdb_run_bz_packaged(const uint64_t *gammas, int n_gammas, const int *
                                const sdb_run_options *opts, sdb_report *report, sdb_trace_entry *trace,
                                int trace_cap, uint64_t *best_out);
 
+/* symdist::BoundsState's per-generation fields (engine.hpp:33-40). */
+typedef struct {
+    long long upper;                          /* in/out; 0 = unset: the sentinel first */
+    unsigned long long candidates_enumerated; /* in/out: += the generation's candidate count */
+    int improved;                             /* out: 1 when a candidate lowered upper */
+} sdb_bounds_state;
+
+/* enumerate_generation(gamma, g, state, filter, workers) (engine.hpp:53-54,
+ * engine.cpp:296-301): every g-combination of ONE matrix (one member row per package; n_packages
+ * = 0 means one package per row, else packages encoded as in sdb_run_bz_packaged) folded into
+ * *state. Candidates below state->upper must pass the filter; the first minimal one (reference
+ * visiting order) is written to best_out (row_words words, Gamma frame) when it improved upper.
+ * Errors as the reference: g outside [1, n_p] or a filter frame other than 2n columns is
+ * SDB_ERR_INVALID_ARGUMENT. The whole generation runs on opts->device (no sharding). */
+sdb_status sdb_enumerate_generation(const uint64_t *gamma, int n_rows, int n_cols, int row_words, int mode,
+                                    int pair_count, int n_packages, const int *packages, int g,
+                                    const uint64_t *filter_rows, int filter_n_rows, int filter_n_cols,
+                                    int filter_row_words, int filter_enabled, int filter_k,
+                                    const sdb_run_options *opts, sdb_bounds_state *state, uint64_t *best_out);
+
 /* lower_bound(g, gammas) for singleton Hamming / symplectic matrices. */
 sdb_status sdb_lower_bound(int g, int mode, int n_gammas, const int *rank_deficits,
                            const int *n_packages, const int *n_pp, long long *out);

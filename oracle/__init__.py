@@ -219,6 +219,35 @@ def ref_run_bz_singleton(mat, mode: str, filter_rows=None, filter_k: int = 0, wo
                 best=best[: blen.value].copy())
 
 
+def ref_enumerate_generation(mat, mode: str, g: int, upper: int = 0, packages=None, filter_rows=None,
+                             filter_k: int = 0, workers: int = 1) -> dict:
+    """The reference's enumerate_generation (engine.hpp:53-54) on one matrix with a bound state
+    entering at `upper` (0: unset) and no best."""
+    lib = _load(REF_SO)
+    a = _u8(mat)
+    if filter_rows is None:
+        f = np.zeros((1, 1), dtype=np.uint8)
+        fr, fc = 0, 0
+    else:
+        f = _u8(filter_rows)
+        fr, fc = f.shape
+    enc = []
+    for pk in packages or []:
+        enc += [len(pk)] + list(pk)
+    enc = np.array(enc or [0], dtype=np.int32)
+    up = C.c_long(upper)
+    cands = C.c_ulonglong(0)
+    best = np.zeros(4096, dtype=np.uint8)
+    blen = C.c_int(0)
+    err = _err()
+    rc = lib.ref_enumerate_generation(_ptr(a), a.shape[0], a.shape[1], 1 if mode == "hamming" else 0,
+                                      len(packages or []), enc.ctypes.data_as(C.POINTER(C.c_int)), g, _ptr(f), fr, fc,
+                                      filter_k, workers, C.byref(up), C.byref(cands), _ptr(best), 4096, C.byref(blen),
+                                      err, 512)
+    _check(rc, err)
+    return dict(upper=up.value, candidates=int(cands.value), best=best[: blen.value].copy())
+
+
 def ref_isometry_best(mat, workers: int = 1) -> dict:
     lib = _load(REF_SO)
     a = _u8(mat)

@@ -304,4 +304,36 @@ int ref_package_best(const uint8_t* bits, int rows, int cols, int alg, int worke
     });
 }
 
+// enumerate_generation (engine.hpp:53-54) on one matrix: singleton_gamma(bits, mode) or, with
+// n_packages > 0, packages encoded as [size, row...] runs; filter rows (filter_rows == 0:
+// disabled); the bound state enters with upper_io (0 = unset) and no best.
+int ref_enumerate_generation(const uint8_t* bits, int rows, int cols, int mode, int n_packages, const int* packages,
+                             int g, const uint8_t* filter_bits, int filter_rows, int filter_cols, int filter_k,
+                             int workers, long* upper_io, unsigned long long* candidates, uint8_t* best, int best_cap,
+                             int* best_len, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        PackagedGamma gamma = singleton_gamma(from_bytes(bits, rows, cols),
+                                              mode ? WeightMode::hamming : WeightMode::symplectic);
+        if (n_packages > 0) {
+            gamma.packages.clear();
+            for (int q = 0, pos = 0; q < n_packages; ++q) {
+                Package pk;
+                const int sz = packages[pos++];
+                for (int i = 0; i < sz; ++i) pk.rows.push_back(packages[pos++]);
+                gamma.packages.push_back(std::move(pk));
+            }
+        }
+        const AdmissibilityFilter filter =
+            filter_rows > 0 ? AdmissibilityFilter::for_rows(from_bytes(filter_bits, filter_rows, filter_cols), filter_k)
+                            : AdmissibilityFilter::disabled();
+        BoundsState st;
+        st.upper = *upper_io;
+        enumerate_generation(gamma, g, st, filter, workers);
+        *upper_io = st.upper;
+        *candidates = st.candidates_enumerated;
+        *best_len = static_cast<int>(st.best.size());
+        for (int i = 0; i < *best_len && i < best_cap; ++i) best[i] = st.best.get(static_cast<std::size_t>(i)) ? 1 : 0;
+    });
+}
+
 }  // extern "C"

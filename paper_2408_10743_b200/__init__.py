@@ -47,7 +47,7 @@ __all__ = [
     "BoundsState", "PackagedGamma", "AdmissibilityFilter", "ValidationResult", "ParseError", "ValidationError",
     "InternalError", "DeviceError", "saved_isometry", "saved_1_gamma", "saved_2_gamma", "compute_distance",
     "diagonalize_f2", "prepare_packages", "random_stabilizer", "parse_matrix_text", "parse_matrix_file",
-    "format_matrix", "cli_path", "Comm", "saved_isometry_batch", "run_bz",
+    "format_matrix", "cli_path", "Comm", "saved_isometry_batch", "run_bz", "enumerate_generation",
     "lower_bound", "validate_normalizer", "isometry_transform", "information_sets", "singleton_gamma",
     "generate_code", "Plan", "pack_rows", "unpack_rows", "library", "library_path", "device_available", "CONFIGS",
 ]
@@ -134,7 +134,7 @@ _EXPORTS = [
     "sdb_isometry_transform", "sdb_information_sets", "sdb_generate_code", "sdb_plan_create", "sdb_plan_run",
     "sdb_plan_destroy", "sdb_saved_1_gamma", "sdb_saved_2_gamma", "sdb_run_bz_packaged", "sdb_prepare_packages",
     "sdb_random_stabilizer", "sdb_parse_matrix_text", "sdb_format_matrix", "sdb_comm_unique_id", "sdb_comm_create",
-    "sdb_comm_destroy", "sdb_comm_allreduce_min",
+    "sdb_comm_destroy", "sdb_comm_allreduce_min", "sdb_enumerate_generation",
 ]
 
 
@@ -569,13 +569,52 @@ class AdmissibilityFilter:
 
 @dataclass
 class BoundsState:
-    lower: int
-    upper: int
-    generation: int
-    candidates_enumerated: int
-    trace: list
-    best: np.ndarray
-    report: DistanceReport
+    """symdist::BoundsState (engine.hpp:33-40); upper = 0 means unset (the sentinel)."""
+    lower: int = 1
+    upper: int = 0
+    generation: int = 0
+    candidates_enumerated: int = 0
+    trace: list = field(default_factory=list)
+    best: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.uint8))
+    report: Optional[DistanceReport] = None
+
+
+class _BoundsC(C.Structure):
+    _fields_ = [("upper", C.c_longlong), ("candidates_enumerated", C.c_ulonglong), ("improved", C.c_int)]
+
+
+def enumerate_generation(gamma: PackagedGamma, g: int, state: BoundsState, filt: AdmissibilityFilter,
+                         workers: int = 1, opts: Optional[RunOptions] = None) -> None:
+    """enumerate_generation (engine.hpp:53-54, engine.cpp:296-301) on the GPU: every g-combination
+    of one matrix (one member per package) folded into `state` — upper (set to the sentinel when
+    0), best (the first minimal codeword, when it improved upper) and candidates_enumerated."""
+    opts = opts or RunOptions(workers=workers)
+    m = np.asarray(gamma.matrix, dtype=np.uint8)
+    rows, cols = m.shape
+    w = pack_rows(m)
+    enc = []
+    for pk in gamma.packages:
+        enc += [len(pk)] + list(pk)
+    enc = np.array(enc or [0], dtype=np.int32)
+    if filt.normalizer is not None and filt.enabled:
+        fw = pack_rows(filt.normalizer)
+        fr, fc, fwords = filt.normalizer.shape[0], filt.normalizer.shape[1], fw.shape[1]
+    else:
+        fw = np.zeros((1, 1), dtype=np.uint64)
+        fr, fc, fwords = 0, 0, 1
+    st = _BoundsC(int(state.upper), int(state.candidates_enumerated), 0)
+    best = np.zeros(w.shape[1], dtype=np.uint64)
+    o, keep = opts._c()
+    rc = library().sdb_enumerate_generation(_wptr(w), rows, cols, w.shape[1], int(gamma.mode), gamma.pair_count,
+                                            len(gamma.packages), enc.ctypes.data_as(C.POINTER(C.c_int)), int(g),
+                                            _wptr(fw), fr, fc, fwords, int(filt.enabled), filt.k if filt.enabled else 0,
+                                            C.byref(o), C.byref(st), _wptr(best))
+    del keep
+    _raise(rc)
+    state.upper = int(st.upper)
+    state.candidates_enumerated = int(st.candidates_enumerated)
+    if st.improved:
+        state.best = unpack_rows(best.reshape(1, -1), cols)[0]
 
 
 def lower_bound(g: int, gammas: Sequence[PackagedGamma]) -> int:

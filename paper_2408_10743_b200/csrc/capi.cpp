@@ -423,6 +423,51 @@ sdb_status sdb_run_bz_packaged(const uint64_t *gammas, int n_gammas, const int *
     });
 }
 
+sdb_status sdb_enumerate_generation(const uint64_t *gamma, int n_rows, int n_cols, int row_words, int mode,
+                                    int pair_count, int n_packages, const int *packages, int g,
+                                    const uint64_t *filter_rows, int filter_n_rows, int filter_n_cols,
+                                    int filter_row_words, int filter_enabled, int filter_k,
+                                    const sdb_run_options *opts, sdb_bounds_state *state, uint64_t *best_out) {
+    return guarded([&] {
+        if (!state) throw sdb::InvalidArgument("null bounds state");
+        if (mode != SDB_MODE_SYMPLECTIC && mode != SDB_MODE_HAMMING) throw sdb::InvalidArgument("unknown weight mode");
+        if (n_packages < 0 || (n_packages > 0 && !packages)) throw sdb::InvalidArgument("null packages");
+        check_matrix_args(gamma, n_rows, n_cols, row_words);
+        state->improved = 0;
+        sdb::GammaIn gm;
+        gm.matrix = sdb::BitMat::from_words(gamma, n_rows, n_cols, row_words);
+        for (int q = 0, pos = 0; q < n_packages; q++) {
+            const int sz = packages[pos++];
+            if (sz < 1 || sz > 3) throw sdb::InvalidArgument("enumerate_generation: packages hold one to three rows");
+            gm.packages.emplace_back(packages + pos, packages + pos + sz);
+            pos += sz;
+        }
+        const int np = n_packages > 0 ? n_packages : n_rows;
+        if (g < 1 || g > np) throw sdb::InvalidArgument("enumerate_generation: generation out of range");
+        sdb::Filter f;
+        f.enabled = filter_enabled && filter_k >= 1;
+        if (f.enabled) {
+            check_matrix_args(filter_rows, filter_n_rows, filter_n_cols, filter_row_words);
+            f.rows = sdb::BitMat::from_words(filter_rows, filter_n_rows, filter_n_cols, filter_row_words);
+        }
+        sdb_run_options o = opts_or_default(opts);
+        o.rank = 0;  // the whole generation on this device
+        o.world = 1;
+        o.comm = nullptr;
+        o.allreduce_min = nullptr;
+        std::vector<sdb::GammaIn> gs;
+        gs.push_back(std::move(gm));
+        sdb::Plan plan(std::move(gs), mode == SDB_MODE_HAMMING ? sdb::Mode::hamming : sdb::Mode::symplectic,
+                       pair_count, f, o);
+        long long upper = state->upper;
+        unsigned long long count = 0;
+        const bool improved = plan.run_level(g, upper, &upper, &count, best_out);
+        state->upper = upper;
+        state->candidates_enumerated += count;
+        state->improved = improved ? 1 : 0;
+    });
+}
+
 sdb_status sdb_lower_bound(int g, int mode, int n_gammas, const int *rank_deficits, const int *n_packages,
                            const int *n_pp, long long *out) {
     return guarded([&] {

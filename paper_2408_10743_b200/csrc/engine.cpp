@@ -865,6 +865,50 @@ void Plan::prepare_level(int g) {
     lv.ready = true;
 }
 
+int Plan::launch_level(int g) {
+    const LevelHost &lv = levels_[size_t(g)];
+    const int nl = lv.t == -2  ? launch_ptile_level(pd_, pk_, pt_, lv.ptile, stream_, num_sms_)
+                   : lv.t == -1 ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
+                   : lv.t == 0  ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
+                                : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
+    if (nl < 0) throw InvalidArgument("unsupported row width");
+    check_cuda(cudaGetLastError(), "level kernel launch");
+    return nl;
+}
+
+bool Plan::run_level(int g, long long upper, long long *upper_out, unsigned long long *candidates,
+                     uint64_t *best_out) {
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    if (G_ != 1) throw InvalidArgument("enumerate_generation: one generator matrix");
+    const int np = packaged_ ? np_[0] : N_;
+    if (g < 1 || g > np) throw InvalidArgument("enumerate_generation: generation out of range");
+    if (g > kMaxLevel) throw InvalidArgument("generation beyond the kernels' combination-size limit");
+    if (upper == 0) upper = sentinel_;  // BoundsState.upper == 0: unset (engine.cpp:299)
+    *candidates = level_candidates(g);
+    *upper_out = upper;
+    if (upper < 0) return false;  // no weight lies below it
+    // every weight is below the sentinel, so a larger incoming bound starts the device at it
+    const unsigned start = unsigned(std::min<long long>(upper, sentinel_));
+    launch_run_init(pd_, start, d_counter_init_, d_counters_, N_ + 1, stream_);
+    check_cuda(cudaGetLastError(), "run init launch");
+    prepare_level(g);
+    launch_level(g);
+    launch_level_close(pd_, g, 0, 0, stream_);  // lower 0: the close never terminates
+    check_cuda(cudaGetLastError(), "level close launch");
+    RunCtl ctl{};
+    check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
+    check_cuda(cudaStreamSynchronize(stream_), "level sync");
+    const bool improved = ctl.best_g == g && (long long)ctl.U < upper;
+    *upper_out = improved ? (long long)ctl.U : upper;
+    if (improved && best_out) {
+        const unsigned long long r = ctl.best_key & ((1ull << kKeyRankBits) - 1);
+        std::vector<uint64_t> acc(size_t(gammas_[0].matrix.stride), 0);
+        unrank_best(g, 0, r, acc);
+        std::copy(acc.begin(), acc.end(), best_out);
+    }
+    return improved;
+}
+
 // The level loop (reference run_bz, engine.cpp:303-343) with the bound state on the device:
 // levels are enqueued without waiting; level_close folds each level into U, writes the
 // trace entry and raises `done` once L(g) >= U, and every later kernel returns at once.
@@ -901,13 +945,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         // per-level events only when the caller wants per-level times; else one pair
         // around all levels (fewer API calls on small codes)
         if (level_seconds || g == 1) check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
-        const int nl = lv.t == -2  ? launch_ptile_level(pd_, pk_, pt_, lv.ptile, stream_, num_sms_)
-                       : lv.t == -1 ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
-                       : lv.t == 0  ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
-                                    : launch_tile_level(pd_, lv.tile, stream_, num_sms_);
-        if (nl < 0) throw InvalidArgument("unsupported row width");
-        launches += nl;
-        check_cuda(cudaGetLastError(), "level kernel launch");
+        launches += launch_level(g);
         int from_keys = 0;
         if (lv.sharded && opts_.comm) {
             // stream-ordered NCCL min-allreduce of the per-weight best keys; level_close reads

@@ -55,6 +55,13 @@ class Plan {
     void run(sdb_report *report, sdb_trace_entry *trace, int trace_cap, uint64_t *best_out,
              double *level_seconds);
 
+    // One generation of a single-matrix plan folded into a bounds state (reference
+    // enumerate_generation, engine.cpp:296-301): candidates with weight below `upper` (the
+    // sentinel when 0) lower it; returns whether one did, the new upper, this generation's
+    // candidate count and, when it improved, the first minimal codeword in the Gamma frame.
+    bool run_level(int g, long long upper, long long *upper_out, unsigned long long *candidates,
+                   uint64_t *best_out);
+
     double h2d_seconds = 0;
     unsigned long long upload_bytes = 0;
     int n_gammas() const { return G_; }
@@ -73,6 +80,7 @@ class Plan {
     };
 
     void upload();
+    int launch_level(int g);  // the level's kernel(s) on the plan's stream; returns the launch count
     long long lower_bound(int g) const;
     void prepare_level(int g);
     bool prepare_ptile(int g, LevelHost &lv, int world, int rank);

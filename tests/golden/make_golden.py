@@ -215,6 +215,52 @@ def package_routes(heavy: bool, workers: int) -> dict:
     return dict(cases=cases, config3_auto=dict(n=c["n"], k=c["k"], codes=batch))
 
 
+def enumerate_generation_cases() -> dict:
+    """The per-level seam enumerate_generation (engine.hpp:53-54) answered by the reference on
+    single matrices: the isometry route's information sets (Hamming mode, filter from the
+    normalizer), the package routes' prepared matrices (symplectic mode, 1- and 3-packages, their
+    routes' filters) and unfiltered symplectic singletons across word boundaries, each entered
+    with upper = 0 (unset), the previous level's bound and a tight bound."""
+    cases = []
+
+    def add(src, m, mode, g, upper, packages=None, frows=None, k=0):
+        r = O.ref_enumerate_generation(m, mode, g, upper=upper, packages=packages, filter_rows=frows, filter_k=k)
+        cases.append(dict(src=src, cols=int(m.shape[1]), matrix=hexrows(m), mode=mode, g=g, upper_in=upper,
+                          packages=packages or [], filter=hexrows(frows) if frows is not None else [],
+                          filter_cols=int(frows.shape[1]) if frows is not None else 0, k=k,
+                          upper=r["upper"], candidates=r["candidates"],
+                          best=hexrows(r["best"].reshape(1, -1))[0] if r["best"].size else ""))
+        return r["upper"]
+
+    codes = [("config1", O.generate(24, 4, 1), 4)]
+    codes += [(f"random n={n} k={k}", O.generate(n, k, 31 + n), k) for n, k in [(12, 3), (20, 2), (30, 4), (40, 1)]]
+    for src, a, k in codes:
+        img = O.ref_isometry_transform(a)
+        for j, gm in enumerate(O.ref_information_sets(img)):
+            up = 0
+            for g in (1, 2, 3):
+                prev = add(f"{src} isometry gamma {j}", gm["matrix"], "hamming", g, up, frows=a, k=k)
+                up = prev
+            add(f"{src} isometry gamma {j} tight", gm["matrix"], "hamming", 3, max(2, up - 4), frows=a, k=k)
+        n = a.shape[1] // 2
+        for alg in ("saved_1_gamma", "saved_2_gamma"):
+            gs = O.ref_prepare_packages(a, alg)
+            for j, gm in enumerate(gs):
+                frows = gm["matrix"][: a.shape[0]] if alg == "saved_1_gamma" else a
+                up = 0
+                for g in (1, 2, 3):
+                    if g > len(gm["packages"]):
+                        break
+                    up = add(f"{src} {alg} gamma {j}", gm["matrix"], "symplectic", g, up, packages=gm["packages"],
+                             frows=frows, k=k)
+    rng = np.random.default_rng(211)
+    for n in (31, 32, 33, 64, 65):
+        m = rng.integers(0, 2, size=(6, 2 * n), dtype=np.uint8)
+        for g in (1, 2, 3):
+            add(f"singleton symplectic n={n}", m, "symplectic", g, 0)
+    return dict(cases=cases)
+
+
 def wide_codes() -> dict:
     """Wide rows (n up to 256: 4-8 u32 words per half, the kernels' upper limit) through the
     first levels of saved_isometry, answered by the reference (levels g <= g_max)."""
@@ -250,6 +296,8 @@ def main() -> None:
         dump("engine_kats.json", engine_kats())
     if want("wide"):
         dump("wide_codes.json", wide_codes())
+    if want("enumgen"):
+        dump("enumerate_generation.json", enumerate_generation_cases())
     if want("packages"):
         dump("package_routes.json", package_routes(args.heavy, args.workers))
     if args.heavy and want("c4"):

@@ -138,3 +138,18 @@ def test_oracle_validation_agrees_with_reference():
     for a in cases:
         ok, _ = O.ref_validate(a)
         assert ok == (O.validate(a) == 0)
+
+
+@ref
+def test_enumerate_generation_golden_matches_live_reference():
+    # the fixture the GPU parity test reads was produced by the reference's own
+    # enumerate_generation; a sample of it is re-answered live here
+    gd = load_golden("enumerate_generation.json")
+    for case in gd["cases"][::7]:
+        m = hex_to_mat(case["matrix"], case["cols"])
+        frows = hex_to_mat(case["filter"], case["filter_cols"]) if case["filter"] else None
+        r = O.ref_enumerate_generation(m, case["mode"], case["g"], upper=case["upper_in"],
+                                       packages=case["packages"] or None, filter_rows=frows, filter_k=case["k"])
+        assert r["upper"] == case["upper"] and r["candidates"] == case["candidates"], case["src"]
+        best = hex_to_mat([case["best"]], case["cols"])[0] if case["best"] else np.zeros(0, np.uint8)
+        assert np.array_equal(r["best"], best), case["src"]
