@@ -830,10 +830,21 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
     uint32_t *s_prows = reinterpret_cast<uint32_t *>(smem + lay.prows);
     __shared__ TileUnit s_un;
     __shared__ unsigned long long s_visited;
+    // units are claimed in runs of consecutive indices (fewer near the end of the level); the
+    // head blocks of one tail chunk are consecutive, so a run mostly reuses the staged tails
+    __shared__ unsigned long long s_claim, s_claim_end;
+    __shared__ int s_restage, s_staged_j, s_staged_b;
+    __shared__ unsigned long long s_staged_t0;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
     for (int i = threadIdx.x; i < G * N * K; i += blockDim.x) s_prows[i] = p.prows[i];
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
-    if (threadIdx.x == 0) s_visited = 0;
+    if (threadIdx.x == 0) {
+        s_visited = 0;
+        s_claim = s_claim_end = 0;
+        s_staged_b = -1;
+    }
+    // this rank's units: local index u is global unit u * world + rank
+    const unsigned long long local_units = (tp.unit_total + tp.shard_world - 1 - tp.shard_rank) / tp.shard_world;
 
     const unsigned sshift = p.scale == 2 ? 1u : 0u;
     const int lane_head = (threadIdx.x >> 5) * (32 * H) + (threadIdx.x & 31) * H;
@@ -841,8 +852,21 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned long long unit = atomicAdd(tp.counter, 1ull) * tp.shard_world + tp.shard_rank;
+            if (s_claim == s_claim_end) {
+#ifndef SDB_UNIT_BATCH
+#define SDB_UNIT_BATCH 4
+#endif
+                // runs of SDB_UNIT_BATCH while plenty remain; single units for the last few
+                // per CTA, which bound the level's tail
+                const unsigned long long seen = *(volatile unsigned long long *)tp.counter;
+                const unsigned long long run =
+                    seen + 4ull * SDB_UNIT_BATCH * gridDim.x < local_units ? SDB_UNIT_BATCH : 1ull;
+                s_claim = atomicAdd(tp.counter, run);
+                s_claim_end = s_claim + run;
+            }
+            const unsigned long long unit = (s_claim++) * tp.shard_world + tp.shard_rank;
             s_un.tcount = 0;
+            s_restage = 0;
             if (unit < tp.unit_total) {
                 // (j, b): the last q with cum[q] <= unit
                 int lo = 0, hi = G * tp.nb - 1;
@@ -854,8 +878,9 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
                 const unsigned long long u = unit - __ldg(tp.cum + lo);
                 const unsigned long long Hb = binom_at(s_binom, BKs, b, tp.h);
                 const unsigned long long Tb = binom_at(s_binom, BKs, N - 1 - b, tp.t - 1);
-                const unsigned long long nT = (Tb + tp.tchunk - 1) / tp.tchunk;
-                const unsigned long long hc = u / nT, tc = u % nT;
+                const unsigned long long nH = (Hb + HB - 1) / HB;
+                // head blocks vary fastest: consecutive units share their tail chunk
+                const unsigned long long tc = u / nH, hc = u % nH;
                 s_un.j = lo / tp.nb;
                 s_un.b = b;
                 s_un.t0 = tc * tp.tchunk;
@@ -863,6 +888,12 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
                 s_un.hbase0 = hc * HB;
                 s_un.pad = int(min((unsigned long long)HB, Hb - hc * HB));  // heads in this block
                 s_visited += (unsigned long long)s_un.pad * (unsigned long long)s_un.tcount;
+                if (s_un.j != s_staged_j || b != s_staged_b || s_un.t0 != s_staged_t0) {
+                    s_restage = 1;
+                    s_staged_j = s_un.j;
+                    s_staged_b = b;
+                    s_staged_t0 = s_un.t0;
+                }
             }
         }
         __syncthreads();
@@ -876,7 +907,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
             // each thread takes a contiguous run and walks it with colex successors
             const int R = (tcount + blockDim.x - 1) / blockDim.x;
             const int i0 = threadIdx.x * R, i1 = min(i0 + R, tcount);
-            if (i0 < i1) {
+            if (s_restage && i0 < i1) {
                 int e[kMaxLevel];
                 unrank_colex(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, BKs, e);
                 uint32_t acc[K];
