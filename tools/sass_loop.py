@@ -25,7 +25,7 @@ for f in re.split(r"\n\s+Function : ", sass):
         body = [o for a, o in ops if tgt <= a <= addr]
         n = sum(o.startswith("POPC") for o in body)
         # the innermost loop that still holds the candidate POPCs (>= 16 per iteration)
-        if n >= 16 and (best is None or len(body) < len(best[1])):
+        if n >= int(__import__("os").environ.get("MIN_POPC", "16")) and (best is None or len(body) < len(best[1])):
             best = (n, body)
     n, body = best
     mix = Counter((o.split()[1] if o.startswith("@") else o.split()[0]).split(".")[0] for o in body)
