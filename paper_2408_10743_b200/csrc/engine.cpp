@@ -582,6 +582,23 @@ cudaEvent_t Plan::level_event(int i) {
 
 size_t tile_smem_bytes(int G, int N, int W, int K, int BK);
 
+// Experiments only: SDB_TILE_FORCE="g:t:tchunk,..." overrides the cost model's (t, tail chunk)
+// for the listed levels (t = 0: the walk / package walk kernel).
+static void forced_tile(int g, int &t, int &tchunk) {
+    const char *force = std::getenv("SDB_TILE_FORCE");
+    if (!force) return;
+    for (const char *q = force; *q;) {
+        int fg = 0, ft = 0, fc = 0, used = 0;
+        if (std::sscanf(q, "%d:%d:%d%n", &fg, &ft, &fc, &used) != 3) break;
+        if (fg == g && ft >= 0 && ft < g && fc >= 2 && fc <= kTailChunk) {
+            t = ft;
+            tchunk = fc;
+        }
+        q += used;
+        if (*q == ',') q++;
+    }
+}
+
 // Cost-model constants of choose_tile, fitted to a (t, tchunk) sweep of config 4 levels 6-8
 // and config 2 levels 4-6 (tools/t_tchunk.py, profiles/r01_tchunk_sweep.log): a unit costs
 // about 40k candidate-equivalents of dispensing, staging and head generation, and the last
@@ -703,6 +720,7 @@ bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
             }
         }
     }
+    forced_tile(g, best_t, best_chunk);
     if (best_t == 0) return false;
     if (ptile_smem_bytes(G_, N_, W_, K_, P_, E_, std::min(BK_, g + 2)) > 200 * 1024) return false;
     PTilePlan &tp = lv.ptile;
@@ -798,15 +816,7 @@ void Plan::prepare_level(int g) {
     if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
     const unsigned long long total = per * (unsigned long long)G_;
     TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_, world);
-    if (const char *force = std::getenv("SDB_TILE_FORCE")) {  // experiments: "g:t:tchunk,..."
-        for (const char *q = force; *q;) {
-            int fg = 0, ft = 0, fc = 0, used = 0;
-            if (std::sscanf(q, "%d:%d:%d%n", &fg, &ft, &fc, &used) != 3) break;
-            if (fg == g && ft >= 0 && ft < g && fc >= 2 && fc <= kTailChunk) tc = TileChoice{ft, fc};
-            q += used;
-            if (*q == ',') q++;
-        }
-    }
+    forced_tile(g, tc.t, tc.tchunk);
     lv.t = tc.t;
     if (lv.t == 0) {
         LevelLaunch &LL = lv.walk;
