@@ -527,10 +527,12 @@ __device__ __forceinline__ void mitm_scan(int g, int G, const unsigned long long
     }
 }
 
-// Each thread takes one contiguous lex-rank segment of the level. The lex order varies the
-// last element fastest, so the hot loop is one row XOR onto the (g-1)-prefix accumulator and
-// one POPC per word; the prefix advances (through the local element array) once per run of
-// last elements. The admissibility syndrome is rebuilt only for candidates below the best.
+// One code per CTA, its whole level loop (U, L, trace, termination) in shared memory. Levels
+// whose meet-in-the-middle lists fit (BatchDev.mitm_g) run mitm_build + mitm_scan; deeper ones
+// fall back to a per-thread walk: each thread takes one contiguous lex-rank segment, and since
+// the lex order varies the last element fastest, its loop is one row XOR onto the (g-1)-prefix
+// accumulator and one POPC per word, the prefix advancing once per run of last elements (the
+// syndrome is rebuilt only for candidates below the best).
 template <int W>
 __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -616,14 +618,8 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
                 v.off = s_moff;
                 T *ent = reinterpret_cast<T *>(s_mitm);
                 unsigned long long *esyn = reinterpret_cast<unsigned long long *>(s_mitm + size_t(b.mitm_cap) * sizeof(T));
-#ifndef SDB_EXP_NOBUILD
                 mitm_build<W>(g, G, N, s_rows, s_syn, SW, s_binom, b.BK, v, ent, esyn, scale, best, wlim);
-#else
-                __syncthreads();
-#endif
-#ifndef SDB_EXP_NOSCAN
                 mitm_scan<W>(g, G, s_binom, b.BK, v, ent, esyn, SW, scale, best, wlim);
-#endif
             }
         }
         // one segment per thread: tiny levels get a candidate or two per thread, not a long
