@@ -531,6 +531,8 @@ void Plan::upload() {
     unsigned char *q = place(nullptr, 0, b_state);
     pd_.state = reinterpret_cast<LevelState *>(q);
     pd_.key_by_w = reinterpret_cast<unsigned long long *>(q + sizeof(LevelState));
+    // the host image's ctl section receives the level checks' D2H copies (pinned: asynchronous)
+    h_ctl_ = reinterpret_cast<RunCtl *>(h_stage_ + at);
     pd_.ctl = reinterpret_cast<RunCtl *>(place(nullptr, 0, b_ctl));
     pd_.trace_upper = reinterpret_cast<int *>(place(nullptr, 0, b_trace));
     d_counters_ = reinterpret_cast<unsigned long long *>(place(nullptr, 0, b_counters));
@@ -944,6 +946,12 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
 #endif
     constexpr int kMaxUncheckedLevels = SDB_MAX_UNCHECKED_LEVELS;
     int launches = 0, last_g = 0, checked_g = 0;
+    // A big level's termination check is deferred: its ctl copy and event are enqueued behind
+    // it, the next level is prepared and enqueued, and only then does the host wait. The
+    // device then never idles on the host's preparation of the next level; a level enqueued
+    // after termination returns at once on the device (RunCtl.done).
+    int pending_g = 0;
+    cudaEvent_t check_ev = level_event(0);
     unsigned long long h2d = 0, d2h = 0;
     launches += launch_run_init(pd_, unsigned(sentinel_), d_counter_init_, d_counters_, N_ + 1, stream_);
     check_cuda(cudaGetLastError(), "run init launch");
@@ -995,13 +1003,25 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         if (level_seconds) check_cuda(cudaEventRecord(level_event(2 * g + 1), stream_), "event");
         last_g = g;
         const unsigned long long total = level_candidates(g);
-        if ((lv.sharded && !opts_.comm) || total >= kSyncCandidates || g == g_limit ||
-            g - checked_g >= kMaxUncheckedLevels) {
-            check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
+        if (pending_g) {
+            // the previous big level's check, now that this level is queued behind it
+            check_cuda(cudaEventSynchronize(check_ev), "level check");
+            checked_g = pending_g;
+            pending_g = 0;
+            if (h_ctl_->done) break;
+        }
+        const bool last = g == g_limit;
+        if (total >= kSyncCandidates && !last && !(lv.sharded && !opts_.comm)) {
+            check_cuda(cudaMemcpyAsync(h_ctl_, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
+            check_cuda(cudaEventRecord(check_ev, stream_), "event");
+            d2h += sizeof ctl;
+            pending_g = g;
+        } else if ((lv.sharded && !opts_.comm) || last || g - checked_g >= kMaxUncheckedLevels) {
+            check_cuda(cudaMemcpyAsync(h_ctl_, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");
             check_cuda(cudaStreamSynchronize(stream_), "level sync");
             d2h += sizeof ctl;
             checked_g = g;
-            if (ctl.done) break;
+            if (h_ctl_->done) break;
         }
         if (!packaged_ && g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
             throw InvalidArgument("generation beyond the kernels' combination-size limit");

@@ -110,6 +110,7 @@ class Plan {
     size_t table_cap_ = 0, table_used_ = 0;
     std::vector<unsigned long long> h_counter_init_;
     unsigned char *h_stage_ = nullptr;         // pinned staging image of the device block
+    RunCtl *h_ctl_ = nullptr;                  // its ctl section: target of the level checks' D2H
     unsigned long long *h_pinned_ = nullptr;  // its unit-table section (table_cap_ entries)
     // package routes
     bool packaged_ = false;
