@@ -131,13 +131,14 @@ SDB_HD constexpr int tile_blocks_per_sm(int K) {
 SDB_HD constexpr int probe_stride(int K) { return (K + 1) & ~1; }
 SDB_HD constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 struct TileSmem {
-    size_t rows, prows, binom, tp, total;
+    size_t rows, prows, adj, binom, tp, total;
 };
 SDB_HD inline TileSmem tile_smem_layout(int G, int N, int W, int K, int BK) {
     TileSmem L{};
     L.rows = 0;
     L.prows = align16(size_t(G) * N * 2 * W * 4);
-    L.binom = align16(L.prows + size_t(G) * N * K * 4);
+    L.adj = align16(L.prows + size_t(G) * N * K * 4);  // prows[r] ^ prows[r + 1]
+    L.binom = align16(L.adj + size_t(G) * N * K * 4);
     L.tp = align16(L.binom + size_t(N + 1) * BK * 8);
     L.total = align16(L.tp + size_t(kTailChunk + 1) * probe_stride(K) * 4);
     return L;

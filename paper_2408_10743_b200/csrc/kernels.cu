@@ -715,6 +715,33 @@ __device__ __forceinline__ void unrank_colex(unsigned long long rho, int m, int 
     }
 }
 
+// log2(i!) for i <= kMaxLevel: the starting estimate of unrank_colex_est
+__constant__ float c_log2fact[kMaxLevel + 1] = {0.0000000f, 0.0000000f, 1.0000000f, 2.5849625f, 4.5849625f, 6.9068906f, 9.4918531f, 12.2992080f, 15.2992080f, 18.4691330f, 21.7910611f, 25.2504927f, 28.8354552f, 32.5358950f, 36.3432499f, 40.2501405f, 44.2501405f, 48.3376033f, 52.5075283f, 56.7554558f, 61.0773839f, 65.4697013f, 69.9291330f, 74.4526949f, 79.0376574f, 83.6815136f, 88.3819533f, 93.1368408f, 97.9441958f, 102.8021767f, 107.7090673f, 112.6632637f, 117.6632637f, 122.7076578f, 127.7951206f, 132.9244036f, 138.0943286f, 143.3037820f, 148.5517095f, 153.8371117f, 159.1590398f, 164.5165918f, 169.9089093f, 175.3351740f, 180.7946056f, 186.2864587f, 191.8100207f, 197.3646095f, 202.9495720f, 208.5642819f, 214.2081381f, 219.8805634f, 225.5810031f, 231.3089236f, 237.0638111f, 242.8451708f, 248.6525257f, 254.4854157f, 260.3433967f, 266.2260398f, 272.1329304f, 278.0636677f, 284.0178640f};
+
+// unrank_colex with each element's search started at an estimate instead of scanning down
+// from the previous element: C(c, i) <= rho < C(c + 1, i) puts c in (x - 1, x + i - 1] with
+// x = (rho * i!)^(1/i), so a start at x + (i - 1)/2 is off by a step or two, where the scan
+// costs up to `lim` dependent shared-memory loads per unrank.
+__device__ __forceinline__ void unrank_colex_est(unsigned long long rho, int m, int lim,
+                                                 const unsigned long long *binom, int BK, int *e) {
+    int c = lim - 1;
+    for (int i = m; i >= 1; i--) {
+        int cc;
+        if (i == 1) {
+            cc = int(min(rho, (unsigned long long)c));  // C(cc, 1) = cc
+        } else {
+            const float lx = (__log2f(float(rho) + 1.0f) + c_log2fact[i]) / float(i);
+            cc = int(exp2f(lx) + 0.5f * float(i - 1));
+            cc = max(min(cc, c), i - 1);
+            while (binom_at(binom, BK, cc, i) > rho) cc--;
+            while (cc < c && binom_at(binom, BK, cc + 1, i) <= rho) cc++;
+        }
+        e[i - 1] = cc;
+        rho -= binom_at(binom, BK, cc, i);
+        c = cc - 1;
+    }
+}
+
 // lexicographic rank of ascending c[0..g-1] among g-subsets of [0, N): the reference's
 // visiting order inside one generation (engine.cpp:202-219)
 __device__ __forceinline__ unsigned long long lexrank(const int *c, int g, int N, const unsigned long long *binom,
@@ -743,9 +770,9 @@ __device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan t
     const int N = p.N, h = tp.h, t = tp.t, g = tp.g, j = un->j, b = un->b;
     const uint32_t *grows = s_rows + j * N * 2 * W;
     int c[kMaxLevel];
-    unrank_colex(un->hbase0 + head_off, h, b, s_binom, BKs, c);
+    unrank_colex_est(un->hbase0 + head_off, h, b, s_binom, BKs, c);
     c[h] = b;
-    unrank_colex(un->t0 + tix, t - 1, N - 1 - b, s_binom, BKs, c + h + 1);
+    unrank_colex_est(un->t0 + tix, t - 1, N - 1 - b, s_binom, BKs, c + h + 1);
     for (int k = h + 1; k < g; k++) c[k] += b + 1;
     uint32_t acc[2 * W];
 #pragma unroll
@@ -833,6 +860,10 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
     __shared__ unsigned long long s_staged_t0;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
     for (int i = threadIdx.x; i < G * N * K; i += blockDim.x) s_prows[i] = p.prows[i];
+    // adjacent-row table: adj[r] = prows[r] ^ prows[r + 1] within each Gamma
+    uint32_t *s_adj = reinterpret_cast<uint32_t *>(smem + lay.adj);
+    for (int i = threadIdx.x; i < G * N * K; i += blockDim.x)
+        s_adj[i] = (i / K) % N < N - 1 ? p.prows[i] ^ p.prows[i + K] : 0u;
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
     if (threadIdx.x == 0) {
         s_visited = 0;
@@ -905,7 +936,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
             const int i0 = threadIdx.x * R, i1 = min(i0 + R, tcount);
             if (s_restage && i0 < i1) {
                 int e[kMaxLevel];
-                unrank_colex(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, BKs, e);
+                unrank_colex_est(s_un.t0 + i0, t - 1, N - 1 - b, s_binom, BKs, e);
                 uint32_t acc[K];
 #pragma unroll
                 for (int w = 0; w < K; w++) acc[w] = pg[b * K + w];
@@ -934,21 +965,38 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
             const uint32_t *pg = s_prows + s_un.j * N * K;
             int e[kMaxLevel];
             uint32_t acc[K];
+            // e0, e1: the two lowest elements in registers (e1 = b for h = 1): most colex
+            // successors just move e0 up by one, one XOR of the adjacent-row table
+            int e0 = 0, e1 = b;
             if (nvalid > 0) {
-                unrank_colex(s_un.hbase0 + lane_head, h, b, s_binom, BKs, e);
+                unrank_colex_est(s_un.hbase0 + lane_head, h, b, s_binom, BKs, e);
 #pragma unroll
                 for (int w = 0; w < K; w++) acc[w] = 0;
                 for (int k = 0; k < h; k++)
 #pragma unroll
                     for (int w = 0; w < K; w++) acc[w] ^= pg[e[k] * K + w];
+                e0 = e[0];
+                if (h > 1) e1 = e[1];
             } else {
                 // lanes without heads: all-ones probe words, the fold never passes the check
 #pragma unroll
                 for (int w = 0; w < K; w++) acc[w] = 0xffffffffu;
             }
+            const uint32_t *ag = s_adj + s_un.j * N * K;
 #pragma unroll
             for (int i = 0; i < H; i++) {
-                if (i > 0 && i < nvalid) colex_step<K>(e, h, acc, pg, 0, K);
+                if (i > 0 && i < nvalid) {
+                    if (e0 + 1 < e1) {
+#pragma unroll
+                        for (int w = 0; w < K; w++) acc[w] ^= ag[e0 * K + w];
+                        e0++;
+                    } else {
+                        e[0] = e0;
+                        colex_step<K>(e, h, acc, pg, 0, K);
+                        e0 = e[0];
+                        e1 = h > 1 ? e[1] : b;
+                    }
+                }
                 // heads past the valid count repeat the last valid head (same candidates)
 #pragma unroll
                 for (int w = 0; w < K; w++) hp[i][w] = acc[w];
