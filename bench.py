@@ -398,12 +398,14 @@ def per_config(P, opts, torch):
     c = P.CONFIGS[3]
     codes = [P.generate_code(c["n"], c["k"], s) for s in c["seeds"]]
     P.saved_isometry_batch(codes, opts)
-    res = P.saved_isometry_batch(codes, opts)
+    runs = [P.saved_isometry_batch(codes, opts) for _ in range(9)]
+    res = sorted(runs, key=lambda x: x.elapsed_seconds)[len(runs) // 2]  # the median run
     hist = {}
     for d in res.distances:
         hist[str(int(d))] = hist.get(str(int(d)), 0) + 1
     out["config3"] = {"codes": len(codes), "codes_per_s_e2e": len(codes) / res.elapsed_seconds,
                       "e2e_ms": 1e3 * res.elapsed_seconds, "device_ms": 1e3 * res.device_seconds,
+                      "runs": len(runs), "statistic": "median of the runs (elapsed normalizers-in-host-memory to results)",
                       "histogram": hist}
     # the package routes on config 4, and the device brute force
     c = P.CONFIGS[4]

@@ -731,8 +731,8 @@ __device__ __forceinline__ void unrank_colex_est(unsigned long long rho, int m, 
             cc = int(min(rho, (unsigned long long)c));  // C(cc, 1) = cc
         } else {
             const float lx = (__log2f(float(rho) + 1.0f) + c_log2fact[i]) / float(i);
-            cc = int(exp2f(lx) + 0.5f * float(i - 1));
-            cc = max(min(cc, c), i - 1);
+            const float est = exp2f(lx) + 0.5f * float(i - 1);
+            cc = max(est >= float(c) ? c : int(est), i - 1);  // clamped before the conversion
             while (binom_at(binom, BK, cc, i) > rho) cc--;
             while (cc < c && binom_at(binom, BK, cc + 1, i) <= rho) cc++;
         }
