@@ -143,15 +143,17 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowlen = 2 * W;
     const int nrow_words = p.G * p.N * rowlen;
+    // rows, syndromes and the binomial columns C(., k < g) the level's unranks read (a small
+    // level would spend most of its time staging the whole table)
+    const int BKs = max(1, min(p.BK, L.g));
     uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem);
-    unsigned long long *s_binom =
-        reinterpret_cast<unsigned long long *>(smem + ((nrow_words * 4 + 15) & ~15));
-    const int nbinom = (p.N + 1) * p.BK;
-    unsigned long long *s_syn = s_binom + nbinom;
+    unsigned long long *s_syn = reinterpret_cast<unsigned long long *>(smem + ((nrow_words * 4 + 15) & ~15));
     const int nsyn = p.G * p.N * p.SW;
+    unsigned long long *s_binom = s_syn + nsyn;
+    const int nbinom = (p.N + 1) * BKs;
     for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) s_rows[i] = p.rows[i];
-    for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[i];
     for (int i = threadIdx.x; i < nsyn; i += blockDim.x) s_syn[i] = p.syn[i];
+    for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
     __syncthreads();
 
     const int g = L.g, N = p.N;
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
         const unsigned long long r1 = min(r0 + L.seg_len, L.per_gamma);
         const uint32_t *grows = s_rows + j * N * rowlen;
         const unsigned long long *gsyn = s_syn + j * N * p.SW;
-        unrank_lex(r0, g, N, s_binom, p.BK, c);
+        unrank_lex(r0, g, N, s_binom, BKs, c);
         uint32_t acc[2 * W];
 #pragma unroll
         for (int i = 0; i < 2 * W; i++) acc[i] = 0;
@@ -702,24 +704,12 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
 
 // ---------------------------------------------------------------- tile: heads x tails
 
-// colex unrank of rho into an m-subset of [0, lim), ascending into e[0..m-1]
-__device__ __forceinline__ void unrank_colex(unsigned long long rho, int m, int lim, const unsigned long long *binom,
-                                             int BK, int *e) {
-    int c = lim - 1;
-    for (int i = m; i >= 1; i--) {
-        unsigned long long v;
-        while ((v = binom_at(binom, BK, c, i)) > rho) c--;
-        e[i - 1] = c;
-        rho -= v;
-        c--;
-    }
-}
-
 // log2(i!) for i <= kMaxLevel: the starting estimate of unrank_colex_est
 __constant__ float c_log2fact[kMaxLevel + 1] = {0.0000000f, 0.0000000f, 1.0000000f, 2.5849625f, 4.5849625f, 6.9068906f, 9.4918531f, 12.2992080f, 15.2992080f, 18.4691330f, 21.7910611f, 25.2504927f, 28.8354552f, 32.5358950f, 36.3432499f, 40.2501405f, 44.2501405f, 48.3376033f, 52.5075283f, 56.7554558f, 61.0773839f, 65.4697013f, 69.9291330f, 74.4526949f, 79.0376574f, 83.6815136f, 88.3819533f, 93.1368408f, 97.9441958f, 102.8021767f, 107.7090673f, 112.6632637f, 117.6632637f, 122.7076578f, 127.7951206f, 132.9244036f, 138.0943286f, 143.3037820f, 148.5517095f, 153.8371117f, 159.1590398f, 164.5165918f, 169.9089093f, 175.3351740f, 180.7946056f, 186.2864587f, 191.8100207f, 197.3646095f, 202.9495720f, 208.5642819f, 214.2081381f, 219.8805634f, 225.5810031f, 231.3089236f, 237.0638111f, 242.8451708f, 248.6525257f, 254.4854157f, 260.3433967f, 266.2260398f, 272.1329304f, 278.0636677f, 284.0178640f};
 
-// unrank_colex with each element's search started at an estimate instead of scanning down
-// from the previous element: C(c, i) <= rho < C(c + 1, i) puts c in (x - 1, x + i - 1] with
+// colex unrank of rho into an m-subset of [0, lim), ascending into e[0..m-1]: for i = m..1 the
+// largest c below the previous element with C(c, i) <= rho. Each search starts at an estimate
+// instead of scanning down from the previous element: C(c, i) <= rho < C(c + 1, i) puts c in (x - 1, x + i - 1] with
 // x = (rho * i!)^(1/i), so a start at x + (i - 1)/2 is off by a step or two, where the scan
 // costs up to `lim` dependent shared-memory loads per unrank.
 __device__ __forceinline__ void unrank_colex_est(unsigned long long rho, int m, int lim,
@@ -1415,9 +1405,13 @@ size_t problem_smem(int G, int N, int W, int SW, int BK) {
     return ((size_t(G) * N * 2 * W * 4 + 15) & ~size_t(15)) + size_t(N + 1) * BK * 8 + size_t(G) * N * SW * 8;
 }
 
+size_t walk_smem(int G, int N, int W, int SW, int BKs) {
+    return ((size_t(G) * N * 2 * W * 4 + 15) & ~size_t(15)) + size_t(G) * N * SW * 8 + size_t(N + 1) * BKs * 8;
+}
+
 template <int W>
 int launch_walk_impl(const ProblemDev &p, const LevelLaunch &L, cudaStream_t st, int num_sms) {
-    const size_t smem = problem_smem(p.G, p.N, W, p.SW, p.BK);
+    const size_t smem = walk_smem(p.G, p.N, W, p.SW, max(1, min(p.BK, L.g)));
     allow_big_smem<walk_kernel<W>>();
     const unsigned long long segs = (L.seg_total + L.shard_world - 1 - L.shard_rank) / L.shard_world;
     const int threads = 256;
