@@ -1061,9 +1061,29 @@ __host__ __device__ inline PtileSmem ptile_layout(int G, int N, int W, int K, in
 }
 
 // colex unrank of rho into m elements with distinct packages inside elements [0, lim):
-// the largest x with F(x, i) <= rho is the i-th element; the rest lie below its package
+// the largest x with F(x, i) <= rho is the i-th element; the rest lie below its package.
+// F(., i) is nondecreasing and F(0, i) = 0, so each element is a binary search (a scan down
+// from the previous element costs up to `lim` dependent shared-memory loads per unrank).
 __device__ __forceinline__ void unrank_pcolex(unsigned long long rho, int m, int lim, const unsigned long long *F,
                                               int BKs, const short *epkg, const short *off, int *e) {
+    int hi = lim - 1;
+    for (int i = m; i >= 1; i--) {
+        int lo = 0;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (F[mid * BKs + i] <= rho) lo = mid; else hi = mid - 1;
+        }
+        e[i - 1] = lo;
+        rho -= F[lo * BKs + i];
+        hi = off[epkg[lo]] - 1;
+    }
+}
+
+// The same unrank scanning down from the bound: the tail staging keeps it, because a tail
+// chunk's first tail mostly sits at the top of its range (measured on config 4's Saved_2_Gamma:
+// bisecting there cost 2%, while bisecting the heads and the rare path gained 0.7%).
+__device__ __forceinline__ void unrank_pcolex_scan(unsigned long long rho, int m, int lim, const unsigned long long *F,
+                                                   int BKs, const short *epkg, const short *off, int *e) {
     int x = lim - 1;
     for (int i = m; i >= 1; i--) {
         while (F[x * BKs + i] > rho) x--;
@@ -1274,7 +1294,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(probe_words(W
                 unsigned long long rest = tau % s_un.tsub;
                 uint32_t acc[K];
                 auto restart = [&]() {
-                    unrank_pcolex(rest, t - 1, s_un.lim_t, v.FR, BKs, v.rpkg, v.roff, e);
+                    unrank_pcolex_scan(rest, t - 1, s_un.lim_t, v.FR, BKs, v.rpkg, v.roff, e);
 #pragma unroll
                     for (int w = 0; w < K; w++) acc[w] = pg[v.erow[v.off[s_un.b] + mb] * K + w];
                     for (int q = 0; q < t - 1; q++)
