@@ -620,7 +620,7 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
     // the dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
     // (measured 1.4e11 vs 3.9e12 cand/s) with perfectly fine granularity.
     const double Hl = heads_per_lane(W), HBk = head_block(W);
-    const double slots = double(num_sms) * tile_blocks_per_sm(W) * std::max(1, world);  // all ranks' CTAs
+    const double slots = double(num_sms) * tile_blocks_per_sm(W, probe_words(W, false)) * std::max(1, world);  // all ranks' CTAs
     std::vector<double> C(size_t(N + 1) * size_t(N + 1), 0.0);  // Pascal's triangle in doubles
     for (int a = 0; a <= N; a++)
         for (int k = 0; k <= a; k++)
@@ -686,7 +686,7 @@ bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
     const unsigned long long total = level_candidates(g);
     if (opts_.kernel != 2 && total < (1ull << 16)) return false;
     const double Hl = heads_per_lane(W_), HBk = head_block(W_);
-    const double slots = double(num_sms_) * tile_blocks_per_sm(W_) * std::max(1, world);
+    const double slots = double(num_sms_) * tile_blocks_per_sm(W_, probe_words(W_, false)) * std::max(1, world);
     double best_time = opts_.kernel == 2 ? 1e300 : double(total) * 28.0 / slots;
     int best_t = 0, best_chunk = kTailChunk;
     auto Hb_of = [&](int j, int b, int h) { return double(F_at(j, h_off_[size_t(j) * (P_ + 1) + b], h)); };
