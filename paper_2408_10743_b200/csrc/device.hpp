@@ -105,19 +105,23 @@ constexpr int kTileThreads = SDB_TILE_THREADS;
 #ifndef SDB_HEADS_W2
 #define SDB_HEADS_W2 8
 #endif
-#ifndef SDB_HEADS_W3
-#define SDB_HEADS_W3 6
+// K = 3 probe words (W = 3, or W = 2 with the extra probe): 6 heads, so 18 head registers
+// fit 4 CTAs/SM
+#ifndef SDB_HEADS_K3
+#define SDB_HEADS_K3 6
 #endif
-SDB_HD constexpr int heads_per_lane(int W) { return W <= 2 ? SDB_HEADS_W2 : W <= 3 ? SDB_HEADS_W3 : (W <= 5 ? 4 : 2); }
-SDB_HD constexpr int head_block(int W) { return kTileThreads * heads_per_lane(W); }
+SDB_HD constexpr int heads_per_lane(int W, int K) {
+    return K == 3 ? SDB_HEADS_K3 : W <= 2 ? SDB_HEADS_W2 : W <= 3 ? 8 : (W <= 5 ? 4 : 2);
+}
+SDB_HD constexpr int head_block(int W, int K) { return kTileThreads * heads_per_lane(W, K); }
 #ifndef SDB_TAIL_CHUNK
 #define SDB_TAIL_CHUNK 1024
 #endif
 constexpr int kTailChunk = SDB_TAIL_CHUNK;
 // resident CTAs per SM (the register cap: 64 registers at 4, 80 at 3), by the head registers
-// per lane, K probe words (W, or W + 1 with the extra probe) x heads_per_lane(W); measured on
-// B200 (profiles/): K <= 2 with 8 heads runs best at 4, K = 3 with 8 heads spills there and
-// runs best at 3, K = 3 with 6 heads (W = 3) runs 1.7% faster at 4 than 8 heads at 3
+// per lane, K probe words (W, or W + 1 with the extra probe) x heads_per_lane(W, K); measured
+// on B200 (profiles/): K <= 2 with 8 heads runs best at 4, K = 3 with 8 heads spills there and
+// runs best at 3, K = 3 with 6 heads (W = 3) runs 1.8% faster at 4 than 8 heads at 3
 #ifndef SDB_TILE_BLOCKS_W2
 #define SDB_TILE_BLOCKS_W2 4
 #endif
@@ -126,7 +130,7 @@ constexpr int kTailChunk = SDB_TAIL_CHUNK;
 #endif
 SDB_HD constexpr int probe_words(int W, bool XP) { return W == 1 ? 2 : W + (XP ? 1 : 0); }
 SDB_HD constexpr int tile_blocks_per_sm(int W, int K) {
-    return (K <= 2 || (K == 3 && heads_per_lane(W) <= 6) ? SDB_TILE_BLOCKS_W2 : SDB_TILE_BLOCKS) *
+    return (K * heads_per_lane(W, K) <= 18 ? SDB_TILE_BLOCKS_W2 : SDB_TILE_BLOCKS) *
            (256 / kTileThreads);
 }
 // Staged tail chunk: the probe words of each tail, [kTailChunk+1][probe_stride(K)] with K =

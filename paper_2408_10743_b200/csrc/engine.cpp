@@ -619,7 +619,8 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
     // padded candidates (every lane of a warp with heads runs H heads) plus kTileUnitCost for
     // the dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
     // (measured 1.4e11 vs 3.9e12 cand/s) with perfectly fine granularity.
-    const double Hl = heads_per_lane(W), HBk = head_block(W);
+    const int K = probe_words(W, false);
+    const double Hl = heads_per_lane(W, K), HBk = head_block(W, K);
     const double slots = double(num_sms) * tile_blocks_per_sm(W, probe_words(W, false)) * std::max(1, world);  // all ranks' CTAs
     std::vector<double> C(size_t(N + 1) * size_t(N + 1), 0.0);  // Pascal's triangle in doubles
     for (int a = 0; a <= N; a++)
@@ -685,7 +686,7 @@ bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
     if (opts_.kernel == 1 || g < 2) return false;
     const unsigned long long total = level_candidates(g);
     if (opts_.kernel != 2 && total < (1ull << 16)) return false;
-    const double Hl = heads_per_lane(W_), HBk = head_block(W_);
+    const double Hl = heads_per_lane(W_, pd_.K), HBk = head_block(W_, pd_.K);
     const double slots = double(num_sms_) * tile_blocks_per_sm(W_, probe_words(W_, false)) * std::max(1, world);
     double best_time = opts_.kernel == 2 ? 1e300 : double(total) * 28.0 / slots;
     int best_t = 0, best_chunk = kTailChunk;
@@ -745,7 +746,7 @@ bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
             if (Hb == 0 || Tb == 0) continue;
             cum.push_back(acc);
             pairs.push_back(unsigned(j) << 16 | unsigned(b));
-            acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
+            acc += ((Hb + head_block(W_, pd_.K) - 1) / head_block(W_, pd_.K)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
         }
     cum.push_back(acc);
     tp.npairs = int(pairs.size());
@@ -853,7 +854,7 @@ void Plan::prepare_level(int g) {
             for (int b = tp.h; b <= N_ - lv.t; b++) {
                 h_table[size_t(j) * tp.nb + (b - tp.h)] = acc;
                 const unsigned long long Hb = binom_u64(b, tp.h), Tb = binom_u64(N_ - 1 - b, lv.t - 1);
-                acc += ((Hb + head_block(W_) - 1) / head_block(W_)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
+                acc += ((Hb + head_block(W_, pd_.K) - 1) / head_block(W_, pd_.K)) * ((Tb + tp.tchunk - 1) / tp.tchunk);
             }
         h_table[size_t(G_) * tp.nb] = acc;
         tp.unit_total = acc;

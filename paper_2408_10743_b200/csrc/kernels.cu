@@ -823,9 +823,9 @@ __device__ __forceinline__ void colex_step(int *e, int m, uint32_t (&acc)[NW], c
 template <int W, bool XP>
 __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_words(W, XP)))
     tile_kernel(ProblemDev p, TilePlan tp) {
-    constexpr int H = heads_per_lane(W);
-    constexpr int HB = head_block(W);
     constexpr int K = probe_words(W, XP);  // probe words per row / head / tail
+    constexpr int H = heads_per_lane(W, K);
+    constexpr int HB = head_block(W, K);
     constexpr int PW = probe_stride(K);
     if (run_done(p)) return;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1203,9 +1203,9 @@ __device__ __noinline__ unsigned ptile_exact(const ProblemDev p, const PkgDev k,
 template <int W, bool XP>
 __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_words(W, XP)))
     ptile_kernel(ProblemDev p, PkgDev k, PtileDev d, PTilePlan tp) {
-    constexpr int H = heads_per_lane(W);
-    constexpr int HB = head_block(W);
     constexpr int K = probe_words(W, XP);
+    constexpr int H = heads_per_lane(W, K);
+    constexpr int HB = head_block(W, K);
     constexpr int PW = probe_stride(K);
     if (run_done(p)) return;
     extern __shared__ __align__(16) unsigned char smem[];
