@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -438,6 +439,13 @@ def per_config(P, opts, torch):
                          "device_levels_ms": 1e3 * r.enum_seconds,
                          "combos_per_s": r.candidates_enumerated / r.enum_seconds,
                          "level_ms": [round(1e3 * x, 3) for x in r.level_seconds]}
+    # the K = 3 tile kernel (W = 3) on its g = 9 launch against the same 1-POPC bound, at the
+    # B200's 1965 MHz SM clock (the clock the main run records under load)
+    import torch
+
+    n_sm = torch.cuda.get_device_properties(opts.device).multi_processor_count
+    g9 = 3 * math.comb(c["n"] + c["k"], 9)
+    out["config5_g9"]["g9_popc_roofline_frac"] = g9 / r.level_seconds[8] / (n_sm * 1965e6 * R_POPC_MEASURED)
     return out
 
 
