@@ -254,6 +254,17 @@ sdb_status sdb_prepare_packages(const uint64_t *rows, int n_rows, int n_cols, in
                                 int *gamma_rows, int *n_packages, int *n_pp, int *packages,
                                 int packages_cap, int *n_gammas);
 
+/* Tensor-core tile kernel encoding (device.hpp TcPlan, csrc/tcenc.cpp), host only: runs the
+ * isometry prep of an (n+k) x 2n normalizer (validation off) when isometry != 0 — else the
+ * matrix itself (2n columns) is the one symplectic-mode Gamma — builds the per-Gamma ±1
+ * coordinates, and checks S * popc(x|z) = C0 + c_h + sum head_k tail_k on `trials` random
+ * head/tail splits per Gamma. *mismatches = failed checks (-1: the code needs more than 128
+ * coordinates, no tensor-core path); k_per_gamma (may be NULL) receives up to max_gammas
+ * coordinate counts, *n_gammas the matrix count. */
+sdb_status sdb_tc_encoding_check(const uint64_t *rows, int n_rows, int n_cols, int row_words, int isometry,
+                                 uint64_t seed, int trials, int *mismatches, int *k_per_gamma,
+                                 int max_gammas, int *n_gammas);
+
 /* BASELINE.md §2 generator: (n+k) x 2n normalizer from seed (xorshift64*), transvections
  * <= 0 means 4n. */
 sdb_status sdb_generate_code(int n, int k, uint64_t seed, int transvections, uint64_t *out,

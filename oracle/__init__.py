@@ -248,8 +248,8 @@ def ref_enumerate_generation(mat, mode: str, g: int, upper: int = 0, packages=No
     return dict(upper=up.value, candidates=int(cands.value), best=best[: blen.value].copy())
 
 
-def ref_isometry_best(mat, workers: int = 1) -> dict:
-    lib = _load(REF_SO)
+def ref_isometry_best(mat, workers: int = 1, native: bool = False) -> dict:
+    lib = _load(REF_NATIVE_SO if native else REF_SO)
     a = _u8(mat)
     best = np.zeros(4096, dtype=np.uint8)
     blen = C.c_int(0)
@@ -288,8 +288,8 @@ def ref_prepare_packages(mat, alg: str) -> list[dict]:
     return res
 
 
-def ref_package_best(mat, alg: str, workers: int = 1) -> dict:
-    lib = _load(REF_SO)
+def ref_package_best(mat, alg: str, workers: int = 1, native: bool = False) -> dict:
+    lib = _load(REF_NATIVE_SO if native else REF_SO)
     a = _u8(mat)
     best = np.zeros(a.shape[1], dtype=np.uint8)
     bl, up = C.c_int(0), C.c_long(0)

@@ -12,6 +12,7 @@
 #include "../../include/symdist_b200.h"
 #include "comm.hpp"
 #include "engine.hpp"
+#include "tcenc.hpp"
 #include "errors.hpp"
 #include "gf2.hpp"
 #include "packages.hpp"
@@ -531,6 +532,30 @@ sdb_status sdb_information_sets(const uint64_t *rows, int n_rows, int n_cols, in
             if (pivots)
                 for (int i = 0; i < n_rows; i++) pivots[size_t(j) * n_rows + i] = is[size_t(j)].pivots[size_t(i)];
         }
+    });
+}
+
+sdb_status sdb_tc_encoding_check(const uint64_t *rows, int n_rows, int n_cols, int row_words, int isometry,
+                                 uint64_t seed, int trials, int *mismatches, int *k_per_gamma, int max_gammas,
+                                 int *n_gammas) {
+    return guarded([&] {
+        check_matrix_args(rows, n_rows, n_cols, row_words);
+        if (n_cols % 2) throw sdb::InvalidArgument("StabilizerInstance: column count must be even and nonzero");
+        const int n = n_cols / 2;
+        const sdb::BitMat a = sdb::BitMat::from_words(rows, n_rows, n_cols, row_words);
+        std::vector<sdb::BitMat> ms;
+        if (isometry) {
+            for (sdb::InfoSet &is : sdb::information_sets(sdb::isometry_transform(a))) ms.push_back(std::move(is.matrix));
+        } else {
+            ms.push_back(a);
+        }
+        std::vector<const sdb::BitMat *> mp;
+        for (const sdb::BitMat &m : ms) mp.push_back(&m);
+        const sdb::TcEncoding enc = sdb::tc_encode(mp, n_rows, n, isometry != 0);
+        if (n_gammas) *n_gammas = int(ms.size());
+        for (int j = 0; k_per_gamma && j < int(enc.gam.size()) && j < max_gammas; j++) k_per_gamma[j] = enc.gam[size_t(j)].K;
+        const int bad = enc.ok ? sdb::tc_selfcheck(enc, mp, n_rows, n, isometry != 0, seed, trials) : -1;
+        if (mismatches) *mismatches = bad;
     });
 }
 

@@ -168,6 +168,75 @@ struct TilePlan {
 };
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms);
 
+// Tensor-core tile kernel (tc_tile_kernel, tc_tile.cuh): the same head x tail units, scored as
+// an int8 GEMM on tcgen05 with the accumulators in TMEM. Per Gamma the host (tcenc.cpp) maps
+// every symbol s to one or three ±1 coordinates so that, for a candidate split into a head
+// S_h and a tail S_t,
+//     S * popc(x|z) = C0 + c_h + sum_k head_k * tail_k
+// exactly: a symbol whose a, b or a^b column is a unit column (one row p holds its 1) is
+// nonzero iff p is chosen or its other component is odd, one coordinate with the component's
+// sign, zeroed on the side that chose p ("mask"), c = alpha * |S ∩ mask rows|; a symbol with
+// no unit column takes three coordinates (a, b, a^b), (3 - sum s_h s_t) / 4. The CTA pipeline
+// (one CTA per SM): 4 producer warps write head tiles (128 x K) and tail tiles (256 x K) to
+// shared memory, one thread issues tcgen05.mma kind::i8 into two 256-column TMEM stages, and 8
+// epilogue warps read the s32 accumulators back as packed 16-bit pairs (tcgen05.ld pack::16b)
+// and keep a running VIMNMX.S16x2 minimum; only a pair at or below the row's threshold takes
+// the exact rare path (tile_exact), so results are bit-identical to the POPC kernels.
+constexpr int kTcHeads = 128;    // heads per head tile (MMA M)
+constexpr int kTcUnitTiles = 8;  // head tiles per unit: a unit holds up to 1024 heads
+constexpr int kTcMaxPart = 10;   // h <= 10 and t - 1 <= 10 (element lists live in registers)
+constexpr int kTcTileN = 256;    // tails per B tile (MMA N)
+constexpr int kTcSlots = 3;      // head tiles in flight
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcProdWarps = 4;
+constexpr int kTcThreads = 32 * (1 + kTcEpiWarps + kTcProdWarps);
+constexpr int kTcMaxK = 128;     // coordinates per operand row
+constexpr int kTcMaxNbt = 6;     // B tiles per unit
+struct TcGammaDev {
+    int K;       // coordinates of this Gamma (multiple of 32; MMA K steps = K / 32)
+    int W1;      // 4-coordinate words whose tail coefficient is alpha (S = 4: 2), the rest 1
+    int C0;      // constant of S * weight
+    int kc;      // the coordinate carrying -c_t on the tail side (head side -1)
+    int S;       // weight scale (2: only unit-column symbols, 4: otherwise)
+    int alpha;   // S / 2
+};
+// One head tile in flight. Head row r of tile a of a unit with na tiles is head rank
+// hbase0 + r * na + a; tail row y of the unit's B tiles is tail rank t0 + (y % 128) * (2 nbt)
+// + y / 128 (each producer thread walks consecutive ranks with colex successors and writes
+// them to rows that keep its stores conflict-free).
+struct TcMeta {
+    unsigned long long hbase0, t0;
+    int j, b, nheads, ntails, nbt, bb, restage, end, a, na;
+    short ch[kTcHeads];  // per head row: alpha * |S_h ∩ mask rows|
+};
+struct TcPlan {
+    TilePlan tile;            // unit table over head blocks of kTcHeads * kTcUnitTiles, tchunk = kTcTileN * nbt
+    int nbt;                  // B tiles per unit
+    int kmax, kw;             // bytes (coordinates) per operand row, sign words per row
+    const uint32_t *sign;     // [G][N][kw] coordinate sign bits (bit 8i + j of word w: coordinate 32w + 4j + i)
+    const short *mask;        // [G][N] coordinate a row masks (-1: none)
+    const TcGammaDev *gam;    // [G]
+};
+struct TcSmem {
+    size_t a, b, sign, mask, rows, binom, meta, gam, cum, total;
+};
+SDB_HD inline TcSmem tc_smem_layout(int G, int N, int W, int kmax, int kw, int nbt, int BKs) {
+    TcSmem L{};
+    L.a = 0;
+    L.b = L.a + size_t(kTcSlots) * kTcHeads * kmax;
+    L.sign = L.b + size_t(2) * nbt * kTcTileN * kmax;
+    L.mask = align16(L.sign + size_t(G) * N * kw * 4);
+    L.rows = align16(L.mask + size_t(G) * N * 2);
+    L.binom = align16(L.rows + size_t(G) * N * 2 * W * 4);
+    L.meta = align16(L.binom + size_t(N + 1) * BKs * 8);
+    L.gam = align16(L.meta + size_t(kTcSlots) * sizeof(TcMeta));
+    L.cum = align16(L.gam + size_t(G) * sizeof(TcGammaDev));       // the level's unit table
+    L.total = align16(L.cum + (size_t(G) * (N + 1) + 1) * 8);
+    return L;
+}
+constexpr size_t kTcSmemMax = 224 * 1024;  // dynamic; the kernel adds ~2 KB of static shared memory
+int launch_tc_level(const ProblemDev &p, const TcPlan &tp, void *stream, int num_sms);
+
 // Package routes (Saved_1_Gamma / Saved_2_Gamma): a level-g
 // candidate picks g packages p_1 < ... < p_g and one member row of each; the reference
 // visits them in lexicographic order of (p_1, m_1, p_2, m_2, ...) (engine.cpp:202-219).

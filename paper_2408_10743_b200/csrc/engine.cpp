@@ -307,6 +307,14 @@ Plan::Plan(std::vector<GammaIn> gammas, Mode mode, int pair_count, const Filter 
     lap("orient");
     SW_ = build_syndromes(gammas_, n, filter, h_syn_);
     lap("syndromes");
+    if (!packaged_ && (mode_ == Mode::symplectic || image_layout_) && W_ <= 4 && n > 0 &&
+        std::getenv("SDB_NO_TC") == nullptr) {
+        std::vector<const BitMat *> mats;
+        for (const GammaIn &g : gammas_) mats.push_back(&g.matrix);
+        tc_enc_ = tc_encode(mats, N_, n, mode_ == Mode::hamming);
+        tc_ok_ = tc_enc_.ok;
+        lap("tc encoding");
+    }
     BK_ = std::min(N_, kMaxLevel) + 2;
     h_binom_ = binom_table(N_, BK_);
     lap("binom");
@@ -508,8 +516,12 @@ void Plan::upload() {
                  b_off = align256(h_off_.size() * 2 + 2), b_F = align256(h_F_.size() * 8 + 8);
     if (packaged_) table_cap_ += size_t(G_) * size_t(P_ + 1) * size_t(P_ + 2);  // room for the pair lists
     const size_t b_tables_pk = align256(table_cap_ * 8);
+    const size_t b_tc_sign = tc_ok_ ? align256(tc_enc_.sign.size() * 4) : 0,
+                 b_tc_mask = tc_ok_ ? align256(tc_enc_.mask.size() * 2) : 0,
+                 b_tc_gam = tc_ok_ ? align256(tc_enc_.gam.size() * sizeof(TcGammaDev)) : 0;
     d_bytes_ = b_prows + b_rows + b_syn + b_binom + b_state + b_ctl + b_trace + 2 * b_counters +
-               (packaged_ ? b_tables_pk + b_pkr + b_pks + b_ws + 4 * b_el + 2 * b_off + 2 * b_F : b_tables);
+               (packaged_ ? b_tables_pk + b_pkr + b_pks + b_ws + 4 * b_el + 2 * b_off + 2 * b_F : b_tables) +
+               b_tc_sign + b_tc_mask + b_tc_gam;
     const auto t0 = std::chrono::steady_clock::now();
     d_mem_ = workspace_get(device_, d_bytes_);
     // every input section is laid out in one pinned staging image of the device block and
@@ -562,6 +574,13 @@ void Plan::upload() {
             throw InvalidArgument("problem too large for shared-memory staging");
     }
     upload_bytes += h_prows_.size() * 4;
+    if (tc_ok_) {
+        d_tc_sign_ = reinterpret_cast<const uint32_t *>(place(tc_enc_.sign.data(), tc_enc_.sign.size() * 4, b_tc_sign));
+        d_tc_mask_ = reinterpret_cast<const short *>(place(tc_enc_.mask.data(), tc_enc_.mask.size() * 2, b_tc_mask));
+        d_tc_gam_ = reinterpret_cast<const TcGammaDev *>(
+            place(tc_enc_.gam.data(), tc_enc_.gam.size() * sizeof(TcGammaDev), b_tc_gam));
+        upload_bytes += tc_enc_.sign.size() * 4 + tc_enc_.mask.size() * 2 + tc_enc_.gam.size() * sizeof(TcGammaDev);
+    }
     check_cuda(cudaMemcpyAsync(base, h_stage_, at, cudaMemcpyHostToDevice, stream_), "H2D plan");
     h2d_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     pd_.G = G_;
@@ -660,6 +679,111 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
 
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel) {
     return choose_tile(G, N, g, W, per_gamma, forced_kernel, 148, 1).t;
+}
+
+// Cost model of the tensor-core tile kernel, in SM cycles per CTA (one CTA per SM). A unit
+// (128 heads x up to 256 nbt tails) costs the larger of its MMAs (128 cycles per 256-column
+// K = 32 step, measured: tools/microbench/tc_i8.cu) and its producer work (the head tile plus
+// its share of the tail staging: a restaged chunk serves the run of units that share it).
+constexpr double kTcHeadTileCycles = 300, kTcTailRowCycles = 3, kTcUnitCycles = 300, kTcEpiCycles = 200;
+TcChoice choose_tc(int G, int N, int g, const std::vector<TcGammaDev> &gam, int kmax, int kw, int W, int BK,
+                   int num_sms, int world) {
+    TcChoice best{0, 1};
+    if (g < 2) return best;
+    const int BKs = std::min(BK, g + 2);
+    int nbt_max = 0;
+    for (int nbt = 1; nbt <= kTcMaxNbt; nbt++)
+        if (tc_smem_layout(G, N, W, kmax, kw, nbt, BKs).total <= kTcSmemMax) nbt_max = nbt;
+    if (nbt_max == 0) return best;
+    std::vector<double> C(size_t(N + 1) * size_t(N + 1), 0.0);
+    for (int a = 0; a <= N; a++)
+        for (int k = 0; k <= a; k++)
+            C[size_t(a) * (N + 1) + size_t(k)] =
+                (k == 0 || k == a) ? 1.0 : C[size_t(a - 1) * (N + 1) + size_t(k - 1)] + C[size_t(a - 1) * (N + 1) + size_t(k)];
+    const double slots = double(num_sms) * std::max(1, world);
+    double best_time = 1e300;
+    const double HB = double(kTcHeads) * kTcUnitTiles;
+    for (int t = std::max(1, g - kTcMaxPart); t < g && t - 1 <= kTcMaxPart; t++) {
+        const int h = g - t;
+        for (int nbt = 1; nbt <= nbt_max; nbt++) {
+            double sum = 0, biggest = 0;
+            for (int j = 0; j < G; j++) {
+                const double kt = gam[size_t(j)].K / 32;
+                for (int b = h; b <= N - t; b++) {
+                    const double Hb = C[size_t(b) * (N + 1) + size_t(h)], Tb = C[size_t(N - 1 - b) * (N + 1) + size_t(t - 1)];
+                    const double nH = std::ceil(Hb / HB), nT = std::ceil(Tb / (kTcTileN * nbt));
+                    const double na = std::ceil(Hb / nH / kTcHeads);    // head tiles per unit
+                    const double tiles = std::ceil(Tb / nT / kTcTileN);  // tail tiles per unit
+                    const double mma = na * tiles * std::max(kt * 128, kTcEpiCycles);
+                    const double restage = nH > 1 ? 1.0 / std::min(nH, 4.0) : 1.0;
+                    const double prod = na * kTcHeadTileCycles + restage * tiles * kTcTileN * kTcTailRowCycles;
+                    const double unit = std::max(mma, prod) + kTcUnitCycles;
+                    sum += nH * nT * unit;
+                    biggest = std::max(biggest, unit);
+                }
+            }
+            const double time = std::max(sum / slots + 0.5 * biggest, biggest);
+            if (time < best_time) {
+                best_time = time;
+                best = TcChoice{t, nbt};
+            }
+        }
+    }
+    return best;
+}
+
+bool Plan::prepare_tc(int g, LevelHost &lv, int world, int rank) {
+    TcChoice c = choose_tc(G_, N_, g, tc_enc_.gam, tc_enc_.kmax, tc_enc_.kw, W_, BK_, num_sms_, world);
+    if (const char *force = std::getenv("SDB_TC_FORCE")) {  // experiments: "g:t:nbt,..."
+        for (const char *q = force; *q;) {
+            int fg = 0, ft = 0, fn = 0, used = 0;
+            if (std::sscanf(q, "%d:%d:%d%n", &fg, &ft, &fn, &used) != 3) break;
+            if (fg == g && ft > 0 && ft < g && fn >= 1 && fn <= kTcMaxNbt) c = TcChoice{ft, fn};
+            q += used;
+            if (*q == ',') q++;
+        }
+    }
+    if (c.t == 0) return false;
+    const int BKs = std::min(BK_, g + 2);
+    if (tc_smem_layout(G_, N_, W_, tc_enc_.kmax, tc_enc_.kw, c.nbt, BKs).total > kTcSmemMax) return false;
+    TcPlan &tp = lv.tc;
+    TilePlan &tl = tp.tile;
+    tl.g = g;
+    tl.t = c.t;
+    tl.h = g - c.t;
+    tl.thr0 = ~0u;
+    tl.nb = N_ - c.t - tl.h + 1;
+    tl.tchunk = kTcTileN * c.nbt;
+    tl.per_gamma = binom_u64(N_, g);
+    const size_t n_entries = size_t(G_) * size_t(tl.nb) + 1;
+    if (table_used_ + n_entries > table_cap_) return false;
+    unsigned long long *h_table = h_pinned_ + table_used_;
+    unsigned long long acc = 0;
+    for (int j = 0; j < G_; j++)
+        for (int b = tl.h; b <= N_ - c.t; b++) {
+            h_table[size_t(j) * tl.nb + (b - tl.h)] = acc;
+            const unsigned long long Hb = binom_u64(b, tl.h), Tb = binom_u64(N_ - 1 - b, c.t - 1);
+            constexpr unsigned long long kHB = kTcHeads * kTcUnitTiles;
+            acc += ((Hb + kHB - 1) / kHB) * ((Tb + tl.tchunk - 1) / tl.tchunk);
+        }
+    h_table[size_t(G_) * tl.nb] = acc;
+    tl.unit_total = acc;
+    tl.shard_rank = rank;
+    tl.shard_world = world;
+    tl.cum = d_tables_ + table_used_;
+    tl.counter = d_counters_ + g;
+    table_used_ += n_entries;
+    check_cuda(cudaMemcpyAsync(const_cast<unsigned long long *>(tl.cum), h_table, n_entries * 8, cudaMemcpyHostToDevice,
+                               stream_),
+               "H2D unit table");
+    tp.nbt = c.nbt;
+    tp.kmax = tc_enc_.kmax;
+    tp.kw = tc_enc_.kw;
+    tp.sign = d_tc_sign_;
+    tp.mask = d_tc_mask_;
+    tp.gam = d_tc_gam_;
+    lv.t = -3;
+    return true;
 }
 
 long long Plan::lower_bound(int g) const {
@@ -818,6 +942,14 @@ void Plan::prepare_level(int g) {
     const unsigned long long per = binom_u64(N_, g);
     if (per >= (1ull << kKeyRankBits)) throw InvalidArgument("level too large for 58-bit combination ranks");
     const unsigned long long total = per * (unsigned long long)G_;
+    if (tc_ok_ && opts_.kernel != 1 && opts_.kernel != 2 && g >= 2 &&
+        (opts_.kernel == 4 || total >= kTcMinCandidates) && prepare_tc(g, lv, world, rank)) {
+        if (std::getenv("SDB_TRACE_HOST"))
+            std::fprintf(stderr, "[sdb] level %d: tensor-core tile t=%d nbt=%d units=%llu sharded=%d\n", g, lv.tc.tile.t,
+                         lv.tc.nbt, (unsigned long long)lv.tc.tile.unit_total, int(lv.sharded));
+        lv.ready = true;
+        return;
+    }
     TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_, world);
     forced_tile(g, tc.t, tc.tchunk);
     lv.t = tc.t;
@@ -880,7 +1012,8 @@ void Plan::prepare_level(int g) {
 
 int Plan::launch_level(int g) {
     const LevelHost &lv = levels_[size_t(g)];
-    const int nl = lv.t == -2  ? launch_ptile_level(pd_, pk_, pt_, lv.ptile, stream_, num_sms_)
+    const int nl = lv.t == -3  ? launch_tc_level(pd_, lv.tc, stream_, num_sms_)
+                   : lv.t == -2 ? launch_ptile_level(pd_, pk_, pt_, lv.ptile, stream_, num_sms_)
                    : lv.t == -1 ? launch_pkg_level(pd_, pk_, lv.pkg, stream_, num_sms_)
                    : lv.t == 0  ? launch_walk_level(pd_, lv.walk, stream_, num_sms_)
                                 : launch_tile_level(pd_, lv.tile, stream_, num_sms_);

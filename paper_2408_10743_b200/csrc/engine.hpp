@@ -11,6 +11,7 @@
 
 #include "device.hpp"
 #include "gf2.hpp"
+#include "tcenc.hpp"
 #include "../../include/symdist_b200.h"
 
 namespace sdb {
@@ -77,6 +78,7 @@ class Plan {
         TilePlan tile{};
         PkgLevel pkg{};
         PTilePlan ptile{};
+        TcPlan tc{};                  // t == -3: tensor-core tile kernel
     };
 
     void upload();
@@ -84,6 +86,7 @@ class Plan {
     long long lower_bound(int g) const;
     void prepare_level(int g);
     bool prepare_ptile(int g, LevelHost &lv, int world, int rank);
+    bool prepare_tc(int g, LevelHost &lv, int world, int rank);
     cudaEvent_t level_event(int i);
 
     std::vector<GammaIn> gammas_;
@@ -112,6 +115,12 @@ class Plan {
     unsigned char *h_stage_ = nullptr;         // pinned staging image of the device block
     RunCtl *h_ctl_ = nullptr;                  // its ctl section: target of the level checks' D2H
     unsigned long long *h_pinned_ = nullptr;  // its unit-table section (table_cap_ entries)
+    // tensor-core tile kernel: coordinate encoding of every Gamma (tcenc.hpp)
+    bool tc_ok_ = false;
+    TcEncoding tc_enc_;
+    const uint32_t *d_tc_sign_ = nullptr;
+    const short *d_tc_mask_ = nullptr;
+    const TcGammaDev *d_tc_gam_ = nullptr;
     // package routes
     bool packaged_ = false;
     int P_ = 0;                                  // package slots per Gamma
@@ -142,6 +151,17 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
 // levels with fewer candidates run whole on every rank (RunOptions.shard_min = 0)
 constexpr unsigned long long kDefaultShardMin = 1ull << 26;
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel);
+
+// Tensor-core levels: the head x tail units on tcgen05 (device.hpp: TcPlan). Levels with at
+// least this many candidates take it when the plan's encoding allows (RunOptions.kernel 0);
+// kernel 4 forces it on every level with g >= 2, kernel 2 forces the POPC tile kernel.
+constexpr unsigned long long kTcMinCandidates = 1ull << 24;
+struct TcChoice {
+    int t;    // 0: not worth it / not possible
+    int nbt;  // B tiles per unit
+};
+TcChoice choose_tc(int G, int N, int g, const std::vector<TcGammaDev> &gam, int kmax, int kw, int W, int BK,
+                   int num_sms, int world);
 
 // Per Gamma and 32-symbol block, swap the x- and z-words of every row so that the word the
 // tile kernel's fast path folds (the first of the block) is the denser one. Weights are

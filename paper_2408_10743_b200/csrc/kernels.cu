@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "device.hpp"
+#include "tc_ptx.cuh"
 
 namespace sdb {
 
@@ -707,6 +708,14 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchDev b) {
 // log2(i!) for i <= kMaxLevel: the starting estimate of unrank_colex_est
 __constant__ float c_log2fact[kMaxLevel + 1] = {0.0000000f, 0.0000000f, 1.0000000f, 2.5849625f, 4.5849625f, 6.9068906f, 9.4918531f, 12.2992080f, 15.2992080f, 18.4691330f, 21.7910611f, 25.2504927f, 28.8354552f, 32.5358950f, 36.3432499f, 40.2501405f, 44.2501405f, 48.3376033f, 52.5075283f, 56.7554558f, 61.0773839f, 65.4697013f, 69.9291330f, 74.4526949f, 79.0376574f, 83.6815136f, 88.3819533f, 93.1368408f, 97.9441958f, 102.8021767f, 107.7090673f, 112.6632637f, 117.6632637f, 122.7076578f, 127.7951206f, 132.9244036f, 138.0943286f, 143.3037820f, 148.5517095f, 153.8371117f, 159.1590398f, 164.5165918f, 169.9089093f, 175.3351740f, 180.7946056f, 186.2864587f, 191.8100207f, 197.3646095f, 202.9495720f, 208.5642819f, 214.2081381f, 219.8805634f, 225.5810031f, 231.3089236f, 237.0638111f, 242.8451708f, 248.6525257f, 254.4854157f, 260.3433967f, 266.2260398f, 272.1329304f, 278.0636677f, 284.0178640f};
 
+// 1 / i for the same i (a multiply instead of a division in the estimate)
+__constant__ float c_inv[kMaxLevel + 1] = {0.0f, 1.0f / 1, 1.0f / 2, 1.0f / 3, 1.0f / 4, 1.0f / 5, 1.0f / 6, 1.0f / 7, 1.0f / 8, 1.0f / 9,
+    1.0f / 10, 1.0f / 11, 1.0f / 12, 1.0f / 13, 1.0f / 14, 1.0f / 15, 1.0f / 16, 1.0f / 17, 1.0f / 18, 1.0f / 19, 1.0f / 20,
+    1.0f / 21, 1.0f / 22, 1.0f / 23, 1.0f / 24, 1.0f / 25, 1.0f / 26, 1.0f / 27, 1.0f / 28, 1.0f / 29, 1.0f / 30, 1.0f / 31,
+    1.0f / 32, 1.0f / 33, 1.0f / 34, 1.0f / 35, 1.0f / 36, 1.0f / 37, 1.0f / 38, 1.0f / 39, 1.0f / 40, 1.0f / 41, 1.0f / 42,
+    1.0f / 43, 1.0f / 44, 1.0f / 45, 1.0f / 46, 1.0f / 47, 1.0f / 48, 1.0f / 49, 1.0f / 50, 1.0f / 51, 1.0f / 52, 1.0f / 53,
+    1.0f / 54, 1.0f / 55, 1.0f / 56, 1.0f / 57, 1.0f / 58, 1.0f / 59, 1.0f / 60, 1.0f / 61, 1.0f / 62};
+
 // colex unrank of rho into an m-subset of [0, lim), ascending into e[0..m-1]: for i = m..1 the
 // largest c below the previous element with C(c, i) <= rho. Each search starts at an estimate
 // instead of scanning down from the previous element: C(c, i) <= rho < C(c + 1, i) puts c in (x - 1, x + i - 1] with
@@ -720,7 +729,7 @@ __device__ __forceinline__ void unrank_colex_est(unsigned long long rho, int m, 
         if (i == 1) {
             cc = int(min(rho, (unsigned long long)c));  // C(cc, 1) = cc
         } else {
-            const float lx = (__log2f(float(rho) + 1.0f) + c_log2fact[i]) / float(i);
+            const float lx = (__log2f(float(rho) + 1.0f) + c_log2fact[i]) * c_inv[i];
             const float est = exp2f(lx) + 0.5f * float(i - 1);
             cc = max(est >= float(c) ? c : int(est), i - 1);  // clamped before the conversion
             while (binom_at(binom, BK, cc, i) > rho) cc--;
@@ -1041,6 +1050,10 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_word
     }
     if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
 }
+
+// ---------------------------------------------------------------- tensor-core tile (tcgen05)
+
+#include "tc_tile.cuh"
 
 // ---------------------------------------------------------------- packaged tile (1/3-packages)
 
@@ -1517,6 +1530,17 @@ int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int
         SDB_TILE_CASE(8)
     }
 #undef SDB_TILE_CASE
+    return -1;
+}
+
+int launch_tc_level(const ProblemDev &p, const TcPlan &tp, void *stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (p.W) {
+        case 1: return launch_tc_impl<1>(p, tp, st, num_sms);
+        case 2: return launch_tc_impl<2>(p, tp, st, num_sms);
+        case 3: return launch_tc_impl<3>(p, tp, st, num_sms);
+        case 4: return launch_tc_impl<4>(p, tp, st, num_sms);
+    }
     return -1;
 }
 

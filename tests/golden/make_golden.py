@@ -273,6 +273,35 @@ def wide_codes() -> dict:
     return dict(cases=cases)
 
 
+def config4_extra(part: str, workers: int) -> dict:
+    """Config 4 answers the full-run fixture (config4.json) leaves out, each from the reference
+    (native build; the results do not depend on the flags):
+      iso_best  - saved_isometry's best codeword with ONE worker (engine.cpp:182-189: the first
+                  minimum in the single-worker visiting order, the one the GPU keys reproduce);
+      s2g       - saved_2_gamma (distance.cpp:115-133): distance, trace, candidates, generations;
+      s2g_best  - saved_2_gamma's best codeword with one worker;
+      s1g_best  - saved_1_gamma's best codeword with one worker (its trace is in package_routes.json).
+    """
+    c = O.CONFIGS[4]
+    a = O.generate(c["n"], c["k"], c["seed"])
+    t0 = time.time()
+    res: dict = dict(config=4, n=c["n"], k=c["k"], seed=c["seed"], part=part)
+    if part == "iso_best":
+        b = O.ref_isometry_best(a, workers=1, native=True)
+        res.update(alg="saved_isometry", best=hexrows([b["best"]])[0], best_len=int(len(b["best"])),
+                   upper=int(b["upper"]))
+    elif part == "s2g":
+        r = O.ref_compute_distance(a, "saved_2_gamma", workers=workers, native=True)
+        res.update(alg="saved_2_gamma", distance=r.distance, trace=r.trace, candidates=r.candidates,
+                   generations=r.generations, ref_elapsed_seconds=r.elapsed_seconds, ref_workers=workers)
+    elif part in ("s2g_best", "s1g_best"):
+        alg = "saved_2_gamma" if part == "s2g_best" else "saved_1_gamma"
+        b = O.ref_package_best(a, alg, workers=1, native=True)
+        res.update(alg=alg, best=hexrows([b["best"]])[0], best_len=int(len(b["best"])), upper=int(b["upper"]))
+    res["wall_seconds"] = time.time() - t0
+    return res
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true", help="also config 4 (full) and config 5 (g<=8)")
@@ -304,6 +333,11 @@ def main() -> None:
         dump("config4.json", single_config(4, args.workers))
     if args.heavy and want("c5"):
         dump("config5_g8.json", single_config(5, args.workers, g_max=8))
+    if args.heavy and want("c5g9"):
+        dump("config5_g9.json", single_config(5, args.workers, g_max=9))
+    for part in ("iso_best", "s2g", "s2g_best", "s1g_best"):
+        if args.heavy and want("c4_" + part):
+            dump(f"config4_{part}.json", config4_extra(part, args.workers))
 
 
 if __name__ == "__main__":
