@@ -177,21 +177,24 @@ int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int
 // nonzero iff p is chosen or its other component is odd, one coordinate with the component's
 // sign, zeroed on the side that chose p ("mask"), c = alpha * |S ∩ mask rows|; a symbol with
 // no unit column takes three coordinates (a, b, a^b), (3 - sum s_h s_t) / 4. The CTA pipeline
-// (one CTA per SM): 4 producer warps write head tiles (128 x K) and tail tiles (256 x K) to
-// shared memory, one thread issues tcgen05.mma kind::i8 into two 256-column TMEM stages, and 8
-// epilogue warps read the s32 accumulators back as packed 16-bit pairs (tcgen05.ld pack::16b)
-// and keep a running VIMNMX.S16x2 minimum; only a pair at or below the row's threshold takes
-// the exact rare path (tile_exact), so results are bit-identical to the POPC kernels.
-constexpr int kTcHeads = 128;    // heads per head tile (MMA M)
-constexpr int kTcUnitTiles = 8;  // head tiles per unit: a unit holds up to 1024 heads
-constexpr int kTcMaxPart = 10;   // h <= 10 and t - 1 <= 10 (element lists live in registers)
-constexpr int kTcTileN = 256;    // tails per B tile (MMA N)
-constexpr int kTcSlots = 3;      // head tiles in flight
+// (one CTA per SM): a unit warp claims units, eight producer warps write their tail tiles (B,
+// double-buffered) and head tiles (A, a ring of four), one thread issues tcgen05.mma
+// kind::i8 into two 256-column TMEM stages, and 8 epilogue warps read the s32 accumulators
+// back as packed 16-bit pairs (tcgen05.ld pack::16b) with a running VIMNMX.S16x2 minimum; only
+// a pair at or below the row's threshold takes the exact rare path (tile_exact), so results
+// are bit-identical to the POPC kernels.
+constexpr int kTcHeads = 128;      // heads per head tile (MMA M)
+constexpr int kTcUnitTiles = 8;    // head tiles per unit: a unit holds up to 1024 heads
+constexpr int kTcMaxPart = 8;      // h <= 8 and t - 1 <= 8 (element lists live in registers)
+constexpr int kTcTileN = 256;      // tails per B tile = MMA N = TMEM columns per stage
+constexpr int kTcStages = 2;       // TMEM stages (512 columns)
+constexpr int kTcProdWarps = 8;    // producer warps: two groups of 4 (alternate head tiles; 128 rows each)
+constexpr int kTcSlots = 4;        // head tiles in flight
+constexpr int kTcUnitQ = 8;        // unit descriptors in flight
 constexpr int kTcEpiWarps = 8;
-constexpr int kTcProdWarps = 4;
-constexpr int kTcThreads = 32 * (1 + kTcEpiWarps + kTcProdWarps);
-constexpr int kTcMaxK = 128;     // coordinates per operand row
-constexpr int kTcMaxNbt = 6;     // B tiles per unit
+constexpr int kTcThreads = 32 * (1 + kTcEpiWarps + 1 + kTcProdWarps);
+constexpr int kTcMaxK = 128;       // coordinates per operand row
+constexpr int kTcMaxNbt = 6;       // B tiles per unit
 struct TcGammaDev {
     int K;       // coordinates of this Gamma (multiple of 32; MMA K steps = K / 32)
     int W1;      // 4-coordinate words whose tail coefficient is alpha (S = 4: 2), the rest 1
@@ -200,13 +203,15 @@ struct TcGammaDev {
     int S;       // weight scale (2: only unit-column symbols, 4: otherwise)
     int alpha;   // S / 2
 };
-// One head tile in flight. Head row r of tile a of a unit with na tiles is head rank
-// hbase0 + r * na + a; tail row y of the unit's B tiles is tail rank t0 + (y % 128) * (2 nbt)
-// + y / 128 (each producer thread walks consecutive ranks with colex successors and writes
-// them to rows that keep its stores conflict-free).
-struct TcMeta {
+// One unit in flight. Head row r of tile a (a < na) is head rank hbase0 + r * na + a; tail
+// row y of the unit's B tiles is tail rank t0 + (y % 256) * nbt + y / 256 (each producer
+// thread walks consecutive ranks with colex successors and writes them to rows that keep its
+// stores conflict-free).
+struct TcUnitDesc {
     unsigned long long hbase0, t0;
-    int j, b, nheads, ntails, nbt, bb, restage, end, a, na;
+    int j, b, nheads, ntails, nbt, na, bb, restage, end, pad;
+};
+struct TcSlotMeta {
     short ch[kTcHeads];  // per head row: alpha * |S_h ∩ mask rows|
 };
 struct TcPlan {
@@ -218,7 +223,7 @@ struct TcPlan {
     const TcGammaDev *gam;    // [G]
 };
 struct TcSmem {
-    size_t a, b, sign, mask, rows, binom, meta, gam, cum, total;
+    size_t a, b, sign, mask, rows, binom, meta, uq, gam, cum, total;
 };
 SDB_HD inline TcSmem tc_smem_layout(int G, int N, int W, int kmax, int kw, int nbt, int BKs) {
     TcSmem L{};
@@ -229,12 +234,13 @@ SDB_HD inline TcSmem tc_smem_layout(int G, int N, int W, int kmax, int kw, int n
     L.rows = align16(L.mask + size_t(G) * N * 2);
     L.binom = align16(L.rows + size_t(G) * N * 2 * W * 4);
     L.meta = align16(L.binom + size_t(N + 1) * BKs * 8);
-    L.gam = align16(L.meta + size_t(kTcSlots) * sizeof(TcMeta));
+    L.uq = align16(L.meta + size_t(kTcSlots) * sizeof(TcSlotMeta));
+    L.gam = align16(L.uq + size_t(kTcUnitQ) * sizeof(TcUnitDesc));
     L.cum = align16(L.gam + size_t(G) * sizeof(TcGammaDev));       // the level's unit table
     L.total = align16(L.cum + (size_t(G) * (N + 1) + 1) * 8);
     return L;
 }
-constexpr size_t kTcSmemMax = 224 * 1024;  // dynamic; the kernel adds ~2 KB of static shared memory
+constexpr size_t kTcSmemMax = 224 * 1024;  // dynamic; the kernel adds ~1 KB of static shared memory
 int launch_tc_level(const ProblemDev &p, const TcPlan &tp, void *stream, int num_sms);
 
 // Package routes (Saved_1_Gamma / Saved_2_Gamma): a level-g

@@ -685,7 +685,7 @@ int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int 
 // (128 heads x up to 256 nbt tails) costs the larger of its MMAs (128 cycles per 256-column
 // K = 32 step, measured: tools/microbench/tc_i8.cu) and its producer work (the head tile plus
 // its share of the tail staging: a restaged chunk serves the run of units that share it).
-constexpr double kTcHeadTileCycles = 300, kTcTailRowCycles = 3, kTcUnitCycles = 300, kTcEpiCycles = 200;
+constexpr double kTcHeadTileCycles = 700, kTcTailRowCycles = 3, kTcUnitCycles = 300, kTcEpiCycles = 200;
 TcChoice choose_tc(int G, int N, int g, const std::vector<TcGammaDev> &gam, int kmax, int kw, int W, int BK,
                    int num_sms, int world) {
     TcChoice best{0, 1};

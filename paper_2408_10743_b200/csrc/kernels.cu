@@ -1536,10 +1536,10 @@ int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int
 int launch_tc_level(const ProblemDev &p, const TcPlan &tp, void *stream, int num_sms) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p.W) {
-        case 1: return launch_tc_impl<1>(p, tp, st, num_sms);
-        case 2: return launch_tc_impl<2>(p, tp, st, num_sms);
-        case 3: return launch_tc_impl<3>(p, tp, st, num_sms);
-        case 4: return launch_tc_impl<4>(p, tp, st, num_sms);
+        case 1: return launch_tc_w<1>(p, tp, st, num_sms);
+        case 2: return launch_tc_w<2>(p, tp, st, num_sms);
+        case 3: return launch_tc_w<3>(p, tp, st, num_sms);
+        case 4: return launch_tc_w<4>(p, tp, st, num_sms);
     }
     return -1;
 }

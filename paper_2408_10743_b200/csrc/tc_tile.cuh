@@ -2,29 +2,37 @@
 // namespace: it shares binom_at, tile_exact, TileUnit, run_done and start_threshold with the
 // POPC tile kernel.
 //
-// Warp roles, one CTA per SM (kTcThreads = 416):
+// Warp roles, one CTA per SM (kTcThreads = 576):
 //   warp 0        TMEM owner (512 columns: two 128 x 256 s32 stages); lane 0 issues the MMAs
 //   warps 1..8    epilogue: tcgen05.ld pack::16b -> packed 16-bit minimum -> threshold test
-//   warps 9..12   producers: claim units, write the tail tiles (B, double-buffered) and the
-//                 head tiles (A, kTcSlots-deep ring) as int8 coordinates in the canonical
-//                 K-major no-swizzle layout (8-row x 16-byte core matrices)
-// Pipelines (mbarriers): A slot full/empty, B buffer full/empty, TMEM stage full/empty.
+//   warp 9        unit warp: claims units and publishes their descriptors
+//   warps 10..17  producers, two groups of four: group g writes the head tiles c with
+//                 c % 2 == g (A, a ring of four; thread r of the group writes row r), and all
+//                 256 threads write the unit's tails (B, two buffers) when its chunk changes —
+//                 int8 coordinates in the canonical K-major no-swizzle layout (8-row x 16-byte
+//                 core matrices)
+// Pipelines (mbarriers): unit queue full/empty, A slot full/empty, B buffer full/empty, TMEM
+// stage full/empty. No CTA-wide barrier after the start: every warp signals its own part, so
+// warps drift freely within the rings.
 //
 // A unit is (Gamma j, boundary b, up to 1024 heads, up to 256 nbt tails): its na <= 8 head
-// tiles each meet all of its nbt tail tiles. Producer thread r owns head row r of every tile
-// of the unit — na consecutive colex ranks, one successor step per tile — and 2 nbt
-// consecutive tails of the unit's chunk, so the element lists stay in registers and no
-// thread unranks more than twice per unit.
+// tiles each meet all of its nbt tail tiles. Head row r of the unit's tiles walks na
+// consecutive colex ranks (successor steps); a producer thread's nbt tails are consecutive
+// ranks too. Element lists stay in registers: the producer routines are compiled per element
+// count (h, t - 1 <= kTcMaxPart) and per sign words per row (KW).
 #pragma once
 
 #include "tc_ptx.cuh"
 
-struct TcUnitInfo {
-    unsigned long long hbase0, t0;
-    int j, b, nheads, ntails, nbt, na, restage, end;
-};
-
-__device__ __forceinline__ void tc_prod_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcProdWarps) : "memory"); }
+#ifdef SDB_TC_PROF
+#define TCP_DECL unsigned long long tcp_t0 = 0, tcp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define TCP_BEGIN tcp_t0 = clock64();
+#define TCP_END(i) tcp_acc[i] += clock64() - tcp_t0;
+#else
+#define TCP_DECL
+#define TCP_BEGIN
+#define TCP_END(i)
+#endif
 
 // 4 coordinates (bytes) of a head: sign bit set -> +1, clear -> -1 (the head carries -s)
 __device__ __forceinline__ uint32_t tc_head_word(uint32_t s, int jj) {
@@ -47,101 +55,196 @@ __device__ __forceinline__ void tc_store_block(unsigned char *tile, int R, int r
     *reinterpret_cast<uint4 *>(d + R * 16) = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
-// colex unrank of rho into an m-subset of [0, lim) (m <= kTcMaxPart), ascending, in registers:
-// the estimate of unrank_colex_est with its loops unrolled over the compile-time bound
-__device__ __forceinline__ void tc_unrank(unsigned long long rho, int m, int lim, const unsigned long long *binom, int BK,
+// colex unrank of rho into an M-subset of [0, lim), ascending, in registers (the estimate of
+// unrank_colex_est, loops unrolled)
+template <int M>
+__device__ __forceinline__ void tc_unrank(unsigned long long rho, int lim, const unsigned long long *binom, int BK,
                                           int (&e)[kTcMaxPart]) {
     int c = lim - 1;
 #pragma unroll
-    for (int i = kTcMaxPart; i >= 1; i--) {
-        if (i <= m) {
-            int cc;
-            if (i == 1) {
-                cc = int(min(rho, (unsigned long long)c));
-            } else {
-                const float lx = (__log2f(float(rho) + 1.0f) + c_log2fact[i]) * c_inv[i];
-                const float est = exp2f(lx) + 0.5f * float(i - 1);
-                cc = max(est >= float(c) ? c : int(est), i - 1);
-                while (binom_at(binom, BK, cc, i) > rho) cc--;
-                while (cc < c && binom_at(binom, BK, cc + 1, i) <= rho) cc++;
-            }
-            e[i - 1] = cc;
-            rho -= binom_at(binom, BK, cc, i);
-            c = cc - 1;
+    for (int i = M; i >= 1; i--) {
+        int cc;
+        if (i == 1) {
+            cc = int(min(rho, (unsigned long long)c));
+        } else {
+            const float lx = (__log2f(float(rho) + 1.0f) + c_log2fact[i]) * c_inv[i];
+            const float est = exp2f(lx) + 0.5f * float(i - 1);
+            cc = max(est >= float(c) ? c : int(est), i - 1);
+            while (binom_at(binom, BK, cc, i) > rho) cc--;
+            while (cc < c && binom_at(binom, BK, cc + 1, i) <= rho) cc++;
         }
+        e[i - 1] = cc;
+        rho -= binom_at(binom, BK, cc, i);
+        c = cc - 1;
     }
 }
 
-// colex successor of the ascending m-subset e (1 <= m <= kTcMaxPart), in registers
-__device__ __forceinline__ void tc_succ(int m, int (&e)[kTcMaxPart]) {
-    int q = m - 1;
+// colex successor of the ascending M-subset e, in registers
+template <int M>
+__device__ __forceinline__ void tc_succ(int (&e)[kTcMaxPart]) {
+    int q = M - 1;
 #pragma unroll
-    for (int k = kTcMaxPart - 2; k >= 0; k--)
-        if (k < m - 1 && e[k] + 1 != e[k + 1]) q = k;
+    for (int k = M - 2; k >= 0; k--)
+        if (e[k] + 1 != e[k + 1]) q = k;
 #pragma unroll
-    for (int k = 0; k < kTcMaxPart; k++) {
+    for (int k = 0; k < M; k++) {
         if (k < q) e[k] = k;
         else if (k == q) e[k]++;
     }
 }
 
-template <int W>
+// sign words and mask count of rows off + e[k] (k < M), plus row `first` when FIRST
+template <int M, int KW, bool FIRST>
+__device__ __forceinline__ void tc_gather(const uint32_t *sg, const short *mk, int off, int first,
+                                          const int (&e)[kTcMaxPart], uint32_t (&sw)[KW], int &cnt) {
+#pragma unroll
+    for (int w = 0; w < KW; w++) sw[w] = FIRST ? sg[first * KW + w] : 0u;
+    cnt = FIRST ? int(mk[first] >= 0) : 0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+        const int rr = off + e[k];
+        cnt += mk[rr] >= 0;
+#pragma unroll
+        for (int w = 0; w < KW; w++) sw[w] ^= sg[rr * KW + w];
+    }
+}
+
+// slot of the c-th head tile of the kernel, and its phase parity
+__device__ __forceinline__ int tc_slot(int c) { return c % kTcSlots; }
+__device__ __forceinline__ uint32_t tc_slot_par(int c) { return (c / kTcSlots) & 1; }
+
+struct TcShared {
+    uint64_t uqfull[kTcUnitQ], uqempty[kTcUnitQ], afull[kTcSlots], aempty[kTcSlots], bfull[2], bempty[2],
+        tfull[kTcStages], tempty[kTcStages];
+};
+
+// Producer thread pq (0..255): this unit's tails pq * nbt .. + nbt - 1 into B rows r * 256 + pq.
+template <int T1, int KW>
+__device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq, int N, int kmax,
+                               const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
+                               unsigned char *buf) {
+    const int b = d.b, R = d.nbt, i0 = pq * R;
+    int e[kTcMaxPart];
+    tc_unrank<T1>(d.t0 + min(i0, d.ntails - 1), N - 1 - b, binom, BKs, e);
+    for (int r = 0; r < R; r++) {
+        if (r > 0 && i0 + r < d.ntails) tc_succ<T1>(e);
+        uint32_t sw[KW];
+        int cnt;
+        tc_gather<T1, KW, true>(sg, mk, b + 1, b, e, sw, cnt);
+        const int y = r * (kTcProdWarps * 32) + pq;  // B row
+        unsigned char *tile = buf + size_t(y / kTcTileN) * kTcTileN * kmax;
+        const int trow = y % kTcTileN;
+#pragma unroll
+        for (int w = 0; w < KW; w++)
+            if (w < gm.K / 32) tc_store_block<false>(tile, kTcTileN, trow, w, sw[w], gm.W1);
+        if (mk[b] >= 0) tile[tc::kmajor_off(kTcTileN, trow, mk[b])] = 0;
+#pragma unroll
+        for (int k = 0; k < T1; k++) {
+            const int cc = mk[b + 1 + e[k]];
+            if (cc >= 0) tile[tc::kmajor_off(kTcTileN, trow, cc)] = 0;
+        }
+        tile[tc::kmajor_off(kTcTileN, trow, gm.kc)] = (unsigned char)(-(gm.alpha * cnt));
+    }
+}
+
+// Producer group g, thread pt (0..127): row pt of the unit's head tiles a with (c0 + a) % 2 == g
+// (c0 = the kernel-wide index of the unit's first tile); returns the tiles this group wrote.
+template <int H, int KW>
+__device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, int pt, int lane, int c0, int kmax,
+                              const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
+                              unsigned char *sA, TcSlotMeta *s_meta, TcShared &sh) {
+    const int r0 = pt * d.na;
+    int e[kTcMaxPart];
+    int a = (g - c0) & 1;  // first tile of this group
+    if (a >= d.na) return 0;
+    tc_unrank<H>(d.hbase0 + min(r0 + a, d.nheads - 1), d.b, binom, BKs, e);
+    const size_t a_slot = size_t(kTcHeads) * kmax;
+    int wrote = 0;
+    for (; a < d.na; a += 2) {
+        if (wrote > 0) {
+            if (r0 + a - 1 < d.nheads) tc_succ<H>(e);
+            if (r0 + a < d.nheads) tc_succ<H>(e);
+        }
+        uint32_t sw[KW];
+        int cnt;
+        tc_gather<H, KW, false>(sg, mk, 0, 0, e, sw, cnt);
+        const int c = c0 + a, s = tc_slot(c);
+        if (lane == 0) tc::mbar_wait(&sh.aempty[s], tc_slot_par(c) ^ 1);
+        __syncwarp();
+        unsigned char *tile = sA + size_t(s) * a_slot;
+#pragma unroll
+        for (int w = 0; w < KW; w++)
+            if (w < gm.K / 32) tc_store_block<true>(tile, kTcHeads, pt, w, sw[w], 0);
+#pragma unroll
+        for (int k = 0; k < H; k++) {
+            const int cc = mk[e[k]];
+            if (cc >= 0) tile[tc::kmajor_off(kTcHeads, pt, cc)] = 0;
+        }
+        s_meta[s].ch[pt] = short(gm.alpha * cnt);
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sh.afull[s]);
+        wrote++;
+    }
+    return wrote;
+}
+
+template <int W, int KW>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, TcPlan tp) {
     if (run_done(p)) return;
     extern __shared__ __align__(1024) unsigned char tc_smem[];
-    __shared__ uint64_t bar_afull[kTcSlots], bar_aempty[kTcSlots], bar_bfull[2], bar_bempty[2], bar_tfull[2],
-        bar_tempty[2];
+    __shared__ TcShared sh;
     __shared__ uint32_t s_tbase;
-    __shared__ unsigned long long s_claim, s_claim_end, s_visited;
-    __shared__ int s_staged_j, s_staged_b;
-    __shared__ unsigned long long s_staged_t0;
-    __shared__ TcUnitInfo s_pu;
+    __shared__ unsigned long long s_visited;
     const TilePlan &tl = tp.tile;
-    const int G = p.G, N = p.N, kmax = tp.kmax, kw = tp.kw;
+    const int G = p.G, N = p.N, kmax = tp.kmax;
     const int BKs = min(p.BK, tl.g + 2);
-    const TcSmem lay = tc_smem_layout(G, N, W, kmax, kw, tp.nbt, BKs);
+    const TcSmem lay = tc_smem_layout(G, N, W, kmax, KW, tp.nbt, BKs);
     unsigned char *smem = tc_smem;
     unsigned char *sA = smem + lay.a, *sB = smem + lay.b;
     uint32_t *s_sign = reinterpret_cast<uint32_t *>(smem + lay.sign);
     short *s_mask = reinterpret_cast<short *>(smem + lay.mask);
     uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem + lay.rows);
     unsigned long long *s_binom = reinterpret_cast<unsigned long long *>(smem + lay.binom);
-    TcMeta *s_meta = reinterpret_cast<TcMeta *>(smem + lay.meta);
+    TcSlotMeta *s_meta = reinterpret_cast<TcSlotMeta *>(smem + lay.meta);
+    TcUnitDesc *s_uq = reinterpret_cast<TcUnitDesc *>(smem + lay.uq);
     TcGammaDev *s_gam = reinterpret_cast<TcGammaDev *>(smem + lay.gam);
     unsigned long long *s_cum = reinterpret_cast<unsigned long long *>(smem + lay.cum);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     for (int i = threadIdx.x; i < G * N * 2 * W; i += blockDim.x) s_rows[i] = p.rows[i];
-    for (int i = threadIdx.x; i < G * N * kw; i += blockDim.x) s_sign[i] = tp.sign[i];
+    for (int i = threadIdx.x; i < G * N * KW; i += blockDim.x) s_sign[i] = tp.sign[i];
     for (int i = threadIdx.x; i < G * N; i += blockDim.x) s_mask[i] = tp.mask[i];
     for (int i = threadIdx.x; i < (N + 1) * BKs; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
     for (int i = threadIdx.x; i < G; i += blockDim.x) s_gam[i] = tp.gam[i];
     for (int i = threadIdx.x; i <= G * tl.nb; i += blockDim.x) s_cum[i] = tl.cum[i];
     if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcUnitQ; s++) {
+            tc::mbar_init(&sh.uqfull[s], 1);
+            tc::mbar_init(&sh.uqempty[s], kTcProdWarps + 1 + kTcEpiWarps);  // producers, MMA thread, epilogue
+        }
         for (int s = 0; s < kTcSlots; s++) {
-            tc::mbar_init(&bar_afull[s], 1);
-            tc::mbar_init(&bar_aempty[s], 1 + kTcEpiWarps);
+            tc::mbar_init(&sh.afull[s], kTcProdWarps / 2);   // the four warps of the writing group
+            tc::mbar_init(&sh.aempty[s], 1 + kTcEpiWarps);   // MMA commit + epilogue (read the slot's meta)
         }
         for (int s = 0; s < 2; s++) {
-            tc::mbar_init(&bar_bfull[s], 1);
-            tc::mbar_init(&bar_bempty[s], 1);
-            tc::mbar_init(&bar_tfull[s], 1);
-            tc::mbar_init(&bar_tempty[s], kTcEpiWarps);
+            tc::mbar_init(&sh.bfull[s], kTcProdWarps);
+            tc::mbar_init(&sh.bempty[s], 1);
+        }
+        for (int s = 0; s < kTcStages; s++) {
+            tc::mbar_init(&sh.tfull[s], 1);
+            tc::mbar_init(&sh.tempty[s], kTcEpiWarps);
         }
         tc::mbar_fence_init();
-        s_claim = s_claim_end = 0;
         s_visited = 0;
-        s_staged_j = -1;
-        s_staged_b = -1;
-        s_staged_t0 = 0;
     }
     if (warp == 0) tc::tmem_alloc(&s_tbase, 512);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = s_tbase;
-    const size_t a_slot = size_t(kTcHeads) * kmax;                // bytes per head tile
-    const size_t b_buf = size_t(tp.nbt) * kTcTileN * kmax;        // bytes per tail buffer
+    const size_t a_slot = size_t(kTcHeads) * kmax;           // bytes per head tile
+    const size_t b_buf = size_t(tp.nbt) * kTcTileN * kmax;   // bytes per tail buffer
 
     if (warp == 0) {
         // ------------------------------------------------------------ MMA issuer
@@ -149,34 +252,53 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             const uint32_t idesc = tc::idesc_i8(kTcHeads, kTcTileN);
             const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB);
             int ts = 0, cur_bb = -1;
-            int uses[2] = {0, 0};
-            for (int it = 0;; it++) {
-                const int s = it % kTcSlots;
-                tc::mbar_wait(&bar_afull[s], (it / kTcSlots) & 1);
-                const TcMeta &m = s_meta[s];
-                if (m.end) break;
-                if (m.restage) {
-                    if (cur_bb >= 0) tc::commit(&bar_bempty[cur_bb]);  // old buffer free once its MMAs finish
-                    cur_bb = m.bb;
-                    tc::mbar_wait(&bar_bfull[cur_bb], uses[cur_bb] & 1);
+            int uses[2] = {0, 0}, c = 0;
+            TCP_DECL
+            const unsigned long long tcp_start = clock64();
+            for (int u = 0;; u++) {
+                TCP_BEGIN
+                tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
+                TCP_END(0)
+                const TcUnitDesc d = s_uq[u % kTcUnitQ];
+                tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+                if (d.end) {
+#ifdef SDB_TC_PROF
+                    if (blockIdx.x == 0) printf("[tcprof] mma: total %llu wait_uq %llu wait_bfull %llu wait_afull %llu wait_tempty %llu stages %d\n", clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3], ts);
+#endif
+                    break;
+                }
+                if (d.restage) {
+                    if (cur_bb >= 0) tc::commit(&sh.bempty[cur_bb]);  // old buffer free once its MMAs finish
+                    cur_bb = d.bb;
+                    TCP_BEGIN
+                    tc::mbar_wait(&sh.bfull[cur_bb], uses[cur_bb] & 1);
+                    TCP_END(1)
                     uses[cur_bb]++;
                 }
-                const int KT = s_gam[m.j].K / 32, nbt = m.nbt;
-                tc::fence_after();
-                const uint32_t a0 = aBase + uint32_t(s * a_slot);
-                for (int nb = 0; nb < nbt; nb++, ts++) {
-                    const int st = ts & 1;
-                    tc::mbar_wait(&bar_tempty[st], ((ts >> 1) & 1) ^ 1);
+                const int KT = s_gam[d.j].K / 32;
+                for (int a = 0; a < d.na; a++, c++) {
+                    const int s = tc_slot(c);
+                    TCP_BEGIN
+                    tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
+                    TCP_END(2)
                     tc::fence_after();
-                    const uint32_t b0 = bBase + uint32_t(cur_bb * b_buf + size_t(nb) * kTcTileN * kmax);
-                    for (int k = 0; k < KT; k++) {
-                        const uint64_t ad = tc::sdesc(a0 + k * 2 * (kTcHeads * 16), kTcHeads * 16, 128);
-                        const uint64_t bd = tc::sdesc(b0 + k * 2 * (kTcTileN * 16), kTcTileN * 16, 128);
-                        tc::mma_i8(tbase + st * kTcTileN, ad, bd, idesc, k > 0);
+                    const uint32_t a0 = aBase + uint32_t(s * a_slot);
+                    for (int nb = 0; nb < d.nbt; nb++, ts++) {
+                        const int st = ts % kTcStages;
+                        TCP_BEGIN
+                        tc::mbar_wait(&sh.tempty[st], ((ts / kTcStages) & 1) ^ 1);
+                        TCP_END(3)
+                        tc::fence_after();
+                        const uint32_t b0 = bBase + uint32_t(cur_bb * b_buf + size_t(nb) * kTcTileN * kmax);
+                        for (int k = 0; k < KT; k++) {
+                            const uint64_t ad = tc::sdesc(a0 + k * 2 * (kTcHeads * 16), kTcHeads * 16, 128);
+                            const uint64_t bd = tc::sdesc(b0 + k * 2 * (kTcTileN * 16), kTcTileN * 16, 128);
+                            tc::mma_i8(tbase + st * kTcTileN, ad, bd, idesc, k > 0);
+                        }
+                        tc::commit(&sh.tfull[st]);
                     }
-                    tc::commit(&bar_tfull[st]);
+                    tc::commit(&sh.aempty[s]);
                 }
-                tc::commit(&bar_aempty[s]);
             }
         }
     } else if (warp <= kTcEpiWarps) {
@@ -187,94 +309,115 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const unsigned sshift = p.scale == 2 ? 1u : 0u;
         unsigned thrH = start_threshold(p, tl.thr0);
         int ts = 0;
-        for (int it = 0;; it++) {
-            const int s = it % kTcSlots;
-            tc::mbar_wait(&bar_afull[s], (it / kTcSlots) & 1);
-            const TcMeta &m = s_meta[s];
-            const int end = m.end;
-            TileUnit un;
-            un.j = m.j;
-            un.b = m.b;
-            un.t0 = m.t0;
-            un.hbase0 = m.hbase0;
-            un.tcount = m.ntails;
-            un.pad = m.nheads;
-            const int nbt = m.nbt;
-            const int hoff = row * m.na + m.a;  // this row's head: rank hbase0 + hoff
-            const int ch = m.ch[row];
+        int c = 0;  // head tiles consumed
+        TCP_DECL
+        const unsigned long long tcp_start = clock64();
+        for (int u = 0;; u++) {
+            TCP_BEGIN
+            tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
+            TCP_END(0)
+            const TcUnitDesc d = s_uq[u % kTcUnitQ];
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&bar_aempty[s]);
-            if (end) break;
-            const TcGammaDev gm = s_gam[un.j];
-            // other CTAs' finds tighten the threshold from the next tile on (the load's latency
-            // overlaps this tile's stages)
-            const unsigned wmin_seen = *(volatile unsigned int *)&p.state->wmin;
-            int T = hoff < un.pad ? gm.S * int(thrH >> sshift) - gm.C0 - ch : -32768;
-            for (int nb = 0; nb < nbt; nb++, ts++) {
-                const int st = ts & 1;
-                tc::mbar_wait(&bar_tfull[st], (ts >> 1) & 1);
-                tc::fence_after();
-                const uint32_t ta = tbase + (uint32_t(32 * q) << 16) + uint32_t(st * kTcTileN + half * 128);
-                uint32_t v0[16], v1[16], v2[16], v3[16];
-                tc::ld16_pack(ta, v0);
-                tc::ld16_pack(ta + 32, v1);
-                tc::ld16_pack(ta + 64, v2);
-                tc::ld16_pack(ta + 96, v3);
-                tc::ld_wait();
-                uint32_t mn = v0[0];
-#pragma unroll
-                for (int i = 1; i < 16; i++) mn = __vmins2(mn, v0[i]);
-#pragma unroll
-                for (int i = 0; i < 16; i++) mn = __vmins2(__vmins2(mn, v1[i]), __vmins2(v2[i], v3[i]));
-                const int lo = int(short(mn & 0xFFFFu)), hi = int(short(mn >> 16));
-                if (min(lo, hi) <= T) {
-                    // rare: the exact path for every pair at or below the threshold
-                    uint32_t all[64];
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        all[i] = v0[i];
-                        all[16 + i] = v1[i];
-                        all[32 + i] = v2[i];
-                        all[48 + i] = v3[i];
-                    }
-                    const int R = 2 * nbt;
-                    for (int x = 0; x < 128; x++) {
-                        const int val = int(short(all[x >> 1] >> (16 * (x & 1))));
-                        if (val > T) continue;
-                        const int y = nb * kTcTileN + half * 128 + x;  // B row -> tail rank offset
-                        const int tix = min((y & 127) * R + (y >> 7), un.tcount - 1);
-                        thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoff, tix, thrH);
-                        T = gm.S * int(thrH >> sshift) - gm.C0 - ch;
-                    }
-                }
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&bar_tempty[st]);
+            if (lane == 0) tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+            if (d.end) {
+#ifdef SDB_TC_PROF
+                if (blockIdx.x == 0 && lane == 0 && (warp == 1 || warp == 5)) printf("[tcprof] epi warp %d: total %llu wait_uq %llu wait_afull %llu wait_tfull %llu work %llu\n", warp, clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3]);
+#endif
+                break;
             }
-            thrH = min(thrH, wmin_seen);
-        }
-    } else {
-        // ------------------------------------------------------------ producers
-        const int pt = threadIdx.x - 32 * (1 + kTcEpiWarps);
-        const unsigned long long local_units = (tl.unit_total + tl.shard_world - 1 - tl.shard_rank) / tl.shard_world;
-        constexpr int kHB = kTcHeads * kTcUnitTiles;  // heads per unit
-        int cur_bb = -1;
-        int fills[2] = {0, 0};
-        int lo = 0;  // (Gamma, b) index of the previous unit (pt == 0): units of a run share it mostly
-        unsigned long long seen = 0;
-        int it = 0;  // head tiles produced
-        for (;;) {
-            if (pt == 0) {
-                TcUnitInfo u{};
-                if (s_claim == s_claim_end) {
-                    const unsigned long long run = seen + 4ull * 4 * gridDim.x < local_units ? 4ull : 1ull;
-                    s_claim = atomicAdd(tl.counter, run);
-                    s_claim_end = s_claim + run;
-                    seen = s_claim + run;
+            const TcGammaDev gm = s_gam[d.j];
+            TileUnit un;
+            un.j = d.j;
+            un.b = d.b;
+            un.t0 = d.t0;
+            un.hbase0 = d.hbase0;
+            un.tcount = d.ntails;
+            un.pad = d.nheads;
+            for (int a = 0; a < d.na; a++, c++) {
+                const int s = tc_slot(c);
+                TCP_BEGIN
+                tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
+                TCP_END(1)
+                const int ch = s_meta[s].ch[row];
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sh.aempty[s]);
+                const int hoff = row * d.na + a;  // this row's head: rank hbase0 + hoff
+                // other CTAs' finds tighten the threshold from the next tile on (the load's
+                // latency overlaps this tile's stages)
+                const unsigned wmin_seen = *(volatile unsigned int *)&p.state->wmin;
+                int T = hoff < d.nheads ? gm.S * int(thrH >> sshift) - gm.C0 - ch : -32768;
+                for (int nb = 0; nb < d.nbt; nb++, ts++) {
+                    const int st = ts % kTcStages;
+                    TCP_BEGIN
+                    tc::mbar_wait(&sh.tfull[st], (ts / kTcStages) & 1);
+                    TCP_END(2)
+                    TCP_BEGIN
+                    tc::fence_after();
+                    const uint32_t ta = tbase + (uint32_t(32 * q) << 16) + uint32_t(st * kTcTileN + half * 128);
+                    uint32_t v[4][16];
+                    tc::ld16_pack(ta, v[0]);
+                    tc::ld16_pack(ta + 32, v[1]);
+                    tc::ld16_pack(ta + 64, v[2]);
+                    tc::ld16_pack(ta + 96, v[3]);
+                    tc::ld_wait();
+                    // tree of packed minimums (short dependency chains)
+                    uint32_t m8[16];
+#pragma unroll
+                    for (int i = 0; i < 16; i++) m8[i] = __vmins2(__vmins2(v[0][i], v[1][i]), __vmins2(v[2][i], v[3][i]));
+#pragma unroll
+                    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                        for (int i = 0; i < w; i++) m8[i] = __vmins2(m8[i], m8[i + w]);
+                    const uint32_t mn = m8[0];
+                    const int lo = int(short(mn & 0xFFFFu)), hi = int(short(mn >> 16));
+                    if (min(lo, hi) <= T) {
+                        // rare: the exact path for every pair at or below the threshold
+                        uint32_t all[64];
+#pragma unroll
+                        for (int i = 0; i < 16; i++) {
+                            all[i] = v[0][i];
+                            all[16 + i] = v[1][i];
+                            all[32 + i] = v[2][i];
+                            all[48 + i] = v[3][i];
+                        }
+                        for (int x = 0; x < 128; x++) {
+                            const int val = int(short(all[x >> 1] >> (16 * (x & 1))));
+                            if (val > T) continue;
+                            const int y = nb * kTcTileN + half * 128 + x;  // B row of the unit
+                            const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
+                                                d.ntails - 1);
+                            thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoff, tix, thrH);
+                            T = gm.S * int(thrH >> sshift) - gm.C0 - ch;
+                        }
+                    }
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&sh.tempty[st]);
+                    TCP_END(3)
                 }
-                const unsigned long long unit = (s_claim++) * tl.shard_world + tl.shard_rank;
-                u.end = unit >= tl.unit_total;
-                if (!u.end) {
+                thrH = min(thrH, wmin_seen);
+            }
+        }
+    } else if (warp == kTcEpiWarps + 1) {
+        // ------------------------------------------------------------ unit warp (lane 0)
+        if (lane == 0) {
+            const unsigned long long local_units =
+                (tl.unit_total + tl.shard_world - 1 - tl.shard_rank) / tl.shard_world;
+            constexpr int kHB = kTcHeads * kTcUnitTiles;  // heads per unit
+            int cur_bb = -1, sj = -1, sb = -1;
+            unsigned long long st0 = 0, claim = 0, claim_end = 0, seen = 0, visited = 0;
+            int lo = 0;  // (Gamma, b) index of the previous unit: units of a run mostly share it
+            for (int u = 0;; u++) {
+                TcUnitDesc d{};
+                if (claim == claim_end) {
+                    const unsigned long long run = seen + 4ull * 4 * gridDim.x < local_units ? 4ull : 1ull;
+                    claim = atomicAdd(tl.counter, run);
+                    claim_end = claim + run;
+                    seen = claim_end;
+                }
+                const unsigned long long unit = (claim++) * tl.shard_world + tl.shard_rank;
+                d.end = unit >= tl.unit_total;
+                if (!d.end) {
                     if (!(s_cum[lo] <= unit && unit < s_cum[lo + 1])) {
                         int l = 0, hi = G * tl.nb - 1;
                         while (l < hi) {
@@ -288,140 +431,72 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     const unsigned long long Hb = binom_at(s_binom, BKs, b, tl.h);
                     const unsigned long long Tb = binom_at(s_binom, BKs, N - 1 - b, tl.t - 1);
                     const unsigned long long nH = (Hb + kHB - 1) / kHB;
-                    const unsigned long long tc = uu / nH, hc = uu % nH;
-                    u.j = lo / tl.nb;
-                    u.b = b;
-                    u.t0 = tc * tl.tchunk;
-                    u.ntails = int(min((unsigned long long)tl.tchunk, Tb - u.t0));
-                    u.nbt = (u.ntails + kTcTileN - 1) / kTcTileN;
-                    u.hbase0 = hc * kHB;
-                    u.nheads = int(min((unsigned long long)kHB, Hb - u.hbase0));
-                    u.na = (u.nheads + kTcHeads - 1) / kTcHeads;
-                    u.restage = u.j != s_staged_j || b != s_staged_b || u.t0 != s_staged_t0;
-                    s_staged_j = u.j;
-                    s_staged_b = b;
-                    s_staged_t0 = u.t0;
-                    s_visited += (unsigned long long)u.nheads * (unsigned long long)u.ntails;
+                    const unsigned long long tcn = uu / nH, hc = uu % nH;
+                    d.j = lo / tl.nb;
+                    d.b = b;
+                    d.t0 = tcn * tl.tchunk;
+                    d.ntails = int(min((unsigned long long)tl.tchunk, Tb - d.t0));
+                    d.nbt = (d.ntails + kTcTileN - 1) / kTcTileN;
+                    d.hbase0 = hc * kHB;
+                    d.nheads = int(min((unsigned long long)kHB, Hb - d.hbase0));
+                    d.na = (d.nheads + kTcHeads - 1) / kTcHeads;
+                    d.restage = d.j != sj || b != sb || d.t0 != st0;
+                    if (d.restage) cur_bb = cur_bb < 0 ? 0 : cur_bb ^ 1;
+                    d.bb = cur_bb;
+                    sj = d.j;
+                    sb = b;
+                    st0 = d.t0;
+                    visited += (unsigned long long)d.nheads * (unsigned long long)d.ntails;
                 }
-                s_pu = u;
+                tc::mbar_wait(&sh.uqempty[u % kTcUnitQ], ((u / kTcUnitQ) & 1) ^ 1);
+                s_uq[u % kTcUnitQ] = d;
+                tc::mbar_arrive(&sh.uqfull[u % kTcUnitQ]);
+                if (d.end) break;
             }
-            tc_prod_sync();
-            const TcUnitInfo u = s_pu;
-            tc_prod_sync();
-            if (u.end) {
-                if (pt == 0) {
-                    const int s = it % kTcSlots;
-                    tc::mbar_wait(&bar_aempty[s], ((it / kTcSlots) & 1) ^ 1);
-                    s_meta[s].end = 1;
-                    tc::mbar_arrive(&bar_afull[s]);
-                }
-                break;
-            }
-            const TcGammaDev gm = s_gam[u.j];
-            const int KT = gm.K / 32;
-            const uint32_t *sg = s_sign + size_t(u.j) * N * kw;
-            const short *mk = s_mask + u.j * N;
-            if (u.restage) {
-                const int bb = cur_bb < 0 ? 0 : cur_bb ^ 1;
-                tc::mbar_wait(&bar_bempty[bb], (fills[bb] & 1) ^ 1);
+            s_visited = visited;
+        }
+    } else {
+        // ------------------------------------------------------------ producers
+        const int pw = warp - (kTcEpiWarps + 2);   // 0..7
+        const int g = pw >> 2;                     // group: head tiles c with c % 2 == g
+        const int pt = 32 * (pw & 3) + lane;       // head row
+        const int pq = 32 * pw + lane;             // tail thread index (0..255)
+        int c0 = 0;                                // kernel-wide index of the unit's first head tile
+        int fills[2] = {0, 0};
+        for (int u = 0;; u++) {
+            tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
+            const TcUnitDesc d = s_uq[u % kTcUnitQ];
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+            if (d.end) break;
+            const TcGammaDev gm = s_gam[d.j];
+            const uint32_t *sg = s_sign + size_t(d.j) * N * KW;
+            const short *mk = s_mask + d.j * N;
+            if (d.restage) {
+                const int bb = d.bb;
+                if (lane == 0) tc::mbar_wait(&sh.bempty[bb], (fills[bb] & 1) ^ 1);
                 fills[bb]++;
-                cur_bb = bb;
-                // tails {b} + colex (t-1)-subsets of (b, N): this thread takes the R = 2 nbt
-                // consecutive ranks t0 + pt R .. and writes rank pt R + r to row r * 128 + pt;
-                // ranks past ntails repeat the last tail (their candidates are duplicates)
+                __syncwarp();
                 unsigned char *buf = sB + size_t(bb) * b_buf;
-                const int t = tl.t, b = u.b;
-                const int R = 2 * u.nbt;
-                const int i0 = pt * R;
-                int e[kTcMaxPart];
-                tc_unrank(u.t0 + min(i0, u.ntails - 1), t - 1, N - 1 - b, s_binom, BKs, e);
-                for (int r = 0; r < R; r++) {
-                    if (r > 0 && i0 + r < u.ntails) tc_succ(t - 1, e);
-                    uint32_t sw[kTcMaxK / 32];
-                    int cnt = mk[b] >= 0;
-#pragma unroll
-                    for (int w = 0; w < kTcMaxK / 32; w++) sw[w] = w < kw ? sg[b * kw + w] : 0u;
-#pragma unroll
-                    for (int k = 0; k < kTcMaxPart; k++)
-                        if (k < t - 1) {
-                            const int rr = b + 1 + e[k];
-                            cnt += mk[rr] >= 0;
-#pragma unroll
-                            for (int w = 0; w < kTcMaxK / 32; w++)
-                                if (w < kw) sw[w] ^= sg[rr * kw + w];
-                        }
-                    const int y = r * kTcHeads + pt;  // B row
-                    unsigned char *tile = buf + size_t(y / kTcTileN) * kTcTileN * kmax;
-                    const int trow = y % kTcTileN;
-#pragma unroll
-                    for (int w = 0; w < kTcMaxK / 32; w++)
-                        if (w < KT) tc_store_block<false>(tile, kTcTileN, trow, w, sw[w], gm.W1);
-                    if (mk[b] >= 0) tile[tc::kmajor_off(kTcTileN, trow, mk[b])] = 0;
-#pragma unroll
-                    for (int k = 0; k < kTcMaxPart; k++)
-                        if (k < t - 1) {
-                            const int c = mk[b + 1 + e[k]];
-                            if (c >= 0) tile[tc::kmajor_off(kTcTileN, trow, c)] = 0;
-                        }
-                    tile[tc::kmajor_off(kTcTileN, trow, gm.kc)] = (unsigned char)(-(gm.alpha * cnt));
+                switch (tl.t - 1) {
+#define SDB_TC_TAILS(m) \
+    case m: tc_write_tails<m, KW>(d, gm, pq, N, kmax, sg, mk, s_binom, BKs, buf); break;
+                    SDB_TC_TAILS(0) SDB_TC_TAILS(1) SDB_TC_TAILS(2) SDB_TC_TAILS(3) SDB_TC_TAILS(4)
+                    SDB_TC_TAILS(5) SDB_TC_TAILS(6) SDB_TC_TAILS(7) SDB_TC_TAILS(8)
+#undef SDB_TC_TAILS
                 }
                 tc::fence_async_smem();
-                tc_prod_sync();
-                if (pt == 0) tc::mbar_arrive(&bar_bfull[bb]);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sh.bfull[bb]);
             }
-            // the unit's head tiles: row pt of tile a is head rank hbase0 + pt * na + a (rows past
-            // nheads repeat the last head; the epilogue ignores them)
-            const int h = tl.h;
-            const int r0 = pt * u.na;
-            int e[kTcMaxPart];
-            tc_unrank(u.hbase0 + min(r0, u.nheads - 1), h, u.b, s_binom, BKs, e);
-            for (int a = 0; a < u.na; a++, it++) {
-                if (a > 0 && r0 + a < u.nheads) tc_succ(h, e);
-                const int s = it % kTcSlots;
-                uint32_t sw[kTcMaxK / 32];
-#pragma unroll
-                for (int w = 0; w < kTcMaxK / 32; w++) sw[w] = 0;
-                int cnt = 0;
-#pragma unroll
-                for (int k = 0; k < kTcMaxPart; k++)
-                    if (k < h) {
-                        cnt += mk[e[k]] >= 0;
-#pragma unroll
-                        for (int w = 0; w < kTcMaxK / 32; w++)
-                            if (w < kw) sw[w] ^= sg[e[k] * kw + w];
-                    }
-                if (pt == 0) tc::mbar_wait(&bar_aempty[s], ((it / kTcSlots) & 1) ^ 1);
-                tc_prod_sync();
-                unsigned char *tile = sA + size_t(s) * a_slot;
-#pragma unroll
-                for (int w = 0; w < kTcMaxK / 32; w++)
-                    if (w < KT) tc_store_block<true>(tile, kTcHeads, pt, w, sw[w], 0);
-#pragma unroll
-                for (int k = 0; k < kTcMaxPart; k++)
-                    if (k < h) {
-                        const int c = mk[e[k]];
-                        if (c >= 0) tile[tc::kmajor_off(kTcHeads, pt, c)] = 0;
-                    }
-                TcMeta &m = s_meta[s];
-                m.ch[pt] = short(gm.alpha * cnt);
-                if (pt == 0) {
-                    m.hbase0 = u.hbase0;
-                    m.t0 = u.t0;
-                    m.j = u.j;
-                    m.b = u.b;
-                    m.nheads = u.nheads;
-                    m.ntails = u.ntails;
-                    m.nbt = u.nbt;
-                    m.bb = cur_bb;
-                    m.restage = a == 0 ? u.restage : 0;
-                    m.end = 0;
-                    m.a = a;
-                    m.na = u.na;
-                }
-                tc::fence_async_smem();
-                tc_prod_sync();
-                if (pt == 0) tc::mbar_arrive(&bar_afull[s]);
+            switch (tl.h) {
+#define SDB_TC_HEADS(m) \
+    case m: tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, sh); break;
+                SDB_TC_HEADS(1) SDB_TC_HEADS(2) SDB_TC_HEADS(3) SDB_TC_HEADS(4)
+                SDB_TC_HEADS(5) SDB_TC_HEADS(6) SDB_TC_HEADS(7) SDB_TC_HEADS(8)
+#undef SDB_TC_HEADS
             }
+            c0 += d.na;
         }
     }
     tc::fence_before();
@@ -430,21 +505,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
 }
 
-template <int W>
+template <int W, int KW>
 int launch_tc_impl(const ProblemDev &p, const TcPlan &tp, cudaStream_t st, int num_sms) {
-    const size_t smem = tc_smem_layout(p.G, p.N, W, tp.kmax, tp.kw, tp.nbt, min(p.BK, tp.tile.g + 2)).total;
+    const size_t smem = tc_smem_layout(p.G, p.N, W, tp.kmax, KW, tp.nbt, min(p.BK, tp.tile.g + 2)).total;
     if (smem > kTcSmemMax) return -1;
     static std::atomic<unsigned long long> done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(done.load() & (1ull << (dev & 63)))) {
-        cudaFuncSetAttribute(tc_tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemMax));
+        cudaFuncSetAttribute(tc_tile_kernel<W, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemMax));
         done.fetch_or(1ull << (dev & 63));
     }
     const unsigned long long units = (tp.tile.unit_total + tp.tile.shard_world - 1 - tp.tile.shard_rank) / tp.tile.shard_world;
     unsigned long long blocks = (unsigned long long)num_sms;
     if (blocks > units) blocks = units;
     if (blocks == 0) return 0;
-    tc_tile_kernel<W><<<unsigned(blocks), kTcThreads, smem, st>>>(p, tp);
+    tc_tile_kernel<W, KW><<<unsigned(blocks), kTcThreads, smem, st>>>(p, tp);
     return 1;
+}
+
+template <int W>
+int launch_tc_w(const ProblemDev &p, const TcPlan &tp, cudaStream_t st, int num_sms) {
+    switch (tp.kw) {
+        case 1: return launch_tc_impl<W, 1>(p, tp, st, num_sms);
+        case 2: return launch_tc_impl<W, 2>(p, tp, st, num_sms);
+        case 3: return launch_tc_impl<W, 3>(p, tp, st, num_sms);
+        case 4: return launch_tc_impl<W, 4>(p, tp, st, num_sms);
+    }
+    return -1;
 }
