@@ -134,7 +134,7 @@ _EXPORTS = [
     "sdb_isometry_transform", "sdb_information_sets", "sdb_generate_code", "sdb_plan_create", "sdb_plan_run",
     "sdb_plan_destroy", "sdb_saved_1_gamma", "sdb_saved_2_gamma", "sdb_run_bz_packaged", "sdb_prepare_packages",
     "sdb_random_stabilizer", "sdb_parse_matrix_text", "sdb_format_matrix", "sdb_comm_unique_id", "sdb_comm_create",
-    "sdb_comm_destroy", "sdb_comm_allreduce_min", "sdb_enumerate_generation",
+    "sdb_comm_destroy", "sdb_comm_allreduce_min", "sdb_enumerate_generation", "sdb_tc_encoding_check",
 ]
 
 
@@ -550,6 +550,23 @@ def information_sets(b) -> list[PackagedGamma]:
         res.append(PackagedGamma(matrix=mat, mode=WeightMode.hamming, pair_count=cols // 3 if cols % 3 == 0 else 0,
                                  rank_deficit=int(defs[j]), pivots=[int(x) for x in piv[j * rows:(j + 1) * rows]]))
     return res
+
+
+def tc_encoding_check(a, isometry: bool = True, seed: int = 1, trials: int = 256):
+    """Host-only check of the tensor-core tile kernel's exact ±1 coordinate encoding
+    (csrc/tcenc.cpp): on `trials` random head/tail splits per Gamma, the encoded dot product
+    must reproduce popc(x|z). Returns (mismatches, [K per Gamma]); mismatches == -1 means the
+    code has no tensor-core encoding (more than 128 coordinates)."""
+    a = np.asarray(a, dtype=np.uint8)
+    rows, cols = a.shape
+    w = pack_rows(a)
+    mism = C.c_int(0)
+    ks = np.zeros(64, dtype=np.int32)
+    ng = C.c_int(0)
+    ip = lambda x: x.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+    _raise(library().sdb_tc_encoding_check(_wptr(w), rows, cols, w.shape[1], int(bool(isometry)), C.c_uint64(seed),
+                                           trials, C.byref(mism), ip(ks), 64, C.byref(ng)))
+    return mism.value, [int(x) for x in ks[:min(ng.value, 64)]]
 
 
 @dataclass

@@ -237,3 +237,19 @@ def test_package_prep_worked_examples():
     assert len(d.packages) == 2 and d.n_pp == 1 and [len(p) for p in d.packages] == [3, 1]
     with pytest.raises(P.ValidationError):
         P.diagonalize_f2(np.array([[1, 0, 0, 1], [1, 0, 0, 1], [0, 0, 1, 1]], dtype=np.uint8))
+
+
+def test_tensor_core_encoding_is_exact_on_the_configs():
+    """The tensor-core tile kernel scores head x tail sums as an int8 dot product of exact ±1
+    coordinates (csrc/tcenc.cpp); the host check compares it with popc(x|z) on random splits."""
+    for i, kexp in ((1, 32), (2, 64), (4, 64), (5, 96)):
+        c = P.CONFIGS[i]
+        a = P.generate_code(c["n"], c["k"], c["seed"])
+        mism, ks = P.tc_encoding_check(a, trials=512)
+        assert mism == 0
+        assert len(ks) == 3 and all(k == kexp for k in ks), ks
+    # random small codes, isometry route and the raw symplectic matrix
+    for seed in range(20):
+        a = P.generate_code(12 + seed % 9, 1 + seed % 4, 500 + seed)
+        assert P.tc_encoding_check(a, trials=128)[0] == 0
+        assert P.tc_encoding_check(a, isometry=False, trials=128)[0] == 0
