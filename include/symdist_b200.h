@@ -106,9 +106,10 @@ typedef struct {
     void *allreduce_ctx;
     int kernel;             /* 0 auto, 1 force the lexicographic-walk kernel (batch: row-major device
                                prep and every level on the per-thread walk, no meet-in-the-middle
-                               lists), 2 force the tile
-                               kernel, 3 batch only: run the prep (validation, information sets) on
-                               the host */
+                               lists), 2 force the POPC head x tail tile kernel, 3 batch only: run
+                               the prep (validation, information sets) on the host, 4 force the
+                               tensor-core tile kernel on every level g >= 2 (auto uses it on
+                               levels of >= 2^24 candidates) */
     void *stream;           /* cudaStream_t to run on (NULL: a private non-blocking stream) */
     void *comm;             /* sdb_comm_create handle (NCCL): with world > 1 the level exchange is a
                                stream-ordered min-allreduce, no host round trip (else allreduce_min) */

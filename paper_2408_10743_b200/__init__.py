@@ -53,8 +53,9 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# SDB_LIBRARY: alternate build of the same library (kernel-variant experiments only)
-_LIB_PATH = os.environ.get("SDB_LIBRARY") or os.path.join(HERE, "libsymdist_b200.so")
+# the product library, built in-tree; tools/ A/B experiments call use_variant_library() explicitly
+IN_TREE_LIBRARY = os.path.join(HERE, "libsymdist_b200.so")
+_LIB_PATH = IN_TREE_LIBRARY
 
 # BASELINE.json configs: (n, k, seed); 3 is the 4096-code batch.
 CONFIGS = {
@@ -140,6 +141,15 @@ _EXPORTS = [
 
 def library_path() -> str:
     return _LIB_PATH
+
+
+def use_variant_library(path: str) -> None:
+    """Kernel-variant A/B experiments only (tools/): load another build of the same C ABI.
+    Must be called before the first library() call; bench.py refuses to run on a variant."""
+    global _LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("use_variant_library: the library is already loaded")
+    _LIB_PATH = os.path.abspath(path)
 
 
 def library():
@@ -245,7 +255,7 @@ class RunOptions:
     rank: int = 0
     world: int = 1
     allreduce_min: Optional[Callable[[np.ndarray], np.ndarray]] = None
-    kernel: int = 0  # 0 auto, 1 walk, 2 tile
+    kernel: int = 0  # 0 auto, 1 walk, 2 POPC tile, 4 tensor-core tile
     stream: int = 0  # cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream); 0 = private
     comm: int = 0  # Comm.handle (NCCL): the level exchange runs on the stream, no host round trip
     shard_min: int = 0  # levels below this many candidates run whole on every rank (0: 2^26)

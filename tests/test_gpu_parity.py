@@ -15,7 +15,9 @@ def tr(rep):
     return [e.astuple() for e in rep.bounds_trace]
 
 
-@pytest.mark.parametrize("kernel", [0, 1, 2])
+# kernel: 0 auto (tensor-core tiles on levels >= 2^24 candidates), 1 lexicographic walk,
+# 2 POPC head x tail tiles, 4 tensor-core tiles on every level g >= 2
+@pytest.mark.parametrize("kernel", [0, 1, 2, 4])
 @pytest.mark.parametrize("name", ["config1.json", "config2.json"])
 def test_small_configs_bit_exact(gpu, name, kernel):
     gd = load_golden(name)
@@ -30,14 +32,18 @@ def test_small_configs_bit_exact(gpu, name, kernel):
     assert (best == hex_to_mat([gd["best"]], gd["best_len"])[0]).all()
 
 
-@pytest.mark.parametrize("kernel", [0, 2])
+@pytest.mark.parametrize("kernel", [0, 2, 4])
 def test_config4_bit_exact(gpu, kernel):
     gd = load_golden("config4.json")
+    gb = load_golden("config4_iso_best.json")  # the single-worker reference's best (engine.cpp:182-189)
     a = hex_to_mat(gd["normalizer"], 2 * gd["n"])
-    rep = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel))
+    rep, best = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel), return_best=True)
     assert rep.distance == gd["distance"] == 10
     assert tr(rep) == [tuple(t) for t in gd["trace"]]
     assert rep.candidates_enumerated == gd["candidates"]
+    assert rep.candidates_visited == rep.candidates_enumerated
+    assert 2 * rep.distance == gb["upper"]
+    assert (best == hex_to_mat([gb["best"]], gb["best_len"])[0]).all()
 
 
 def test_config5_first_eight_levels_bit_exact(gpu):
@@ -47,6 +53,18 @@ def test_config5_first_eight_levels_bit_exact(gpu):
     assert not rep.complete
     assert tr(rep) == [tuple(t) for t in gd["trace"]]
     assert rep.candidates_enumerated == sum(gd["level_candidates"])
+
+
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_config5_first_nine_levels_bit_exact(gpu, kernel):
+    # g = 9 alone is 2.1e12 candidates, 99.99% of the levels through g = 9; the reference
+    # (native build, 6 workers) took 2066 s on it (tests/golden/config5_g9.json)
+    gd = load_golden("config5_g9.json")
+    a = hex_to_mat(gd["normalizer"], 2 * gd["n"])
+    rep = gpu.saved_isometry(a, gpu.RunOptions(kernel=kernel, max_generation=9))
+    assert not rep.complete
+    assert tr(rep) == [tuple(t) for t in gd["trace"]]
+    assert rep.candidates_enumerated == rep.candidates_visited == sum(gd["level_candidates"])
 
 
 def test_batch_config3_bit_exact(gpu):

@@ -116,7 +116,7 @@ def test_nccl_exchange_path_on_one_gpu(gpu):
 
 
 def test_config5_through_g10_matches_the_full_run(gpu):
-    # levels g <= 8 are pinned to the reference (config5_g8.json); g = 9, 10 against this
+    # levels g <= 9 are pinned to the reference (config5_g9.json); g = 10 against this
     # build's own complete run (profiles/r01_config5_full.json: d = 14 after 13 levels), which
     # no CPU can reproduce (SURVEY.md §0 finding 3) — a determinism and monotonicity check
     c = gpu.CONFIGS[5]
