@@ -140,7 +140,9 @@ typedef struct {
     unsigned long long best_rank;        /* its lexicographic rank inside that level/Gamma */
     unsigned long long h2d_bytes;        /* host->device bytes this call moved */
     unsigned long long d2h_bytes;        /* device->host bytes this call moved */
-    int reserved[4];
+    int last_level_kernel;               /* kernel of the last level run: 1 walk, 2 POPC tile,
+                                            3 tensor-core tile, 4 package walk, 5 package tile */
+    int reserved[3];
 } sdb_report;
 
 void sdb_default_options(sdb_run_options *opts);

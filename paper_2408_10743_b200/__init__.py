@@ -123,7 +123,7 @@ class _Report(C.Structure):
         ("candidates_visited", C.c_ulonglong), ("prep_seconds", C.c_double), ("enum_seconds", C.c_double),
         ("n_gammas", C.c_int), ("kernel_launches", C.c_int), ("best_generation", C.c_int), ("best_gamma", C.c_int),
         ("best_rank", C.c_ulonglong), ("h2d_bytes", C.c_ulonglong), ("d2h_bytes", C.c_ulonglong),
-        ("reserved", C.c_int * 4),
+        ("last_level_kernel", C.c_int), ("reserved", C.c_int * 3),
     ]
 
 
@@ -323,6 +323,7 @@ class DistanceReport:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     level_seconds: list = field(default_factory=list)
+    last_level_kernel: int = 0  # 1 walk, 2 POPC tile, 3 tensor-core tile, 4 package walk, 5 package tile
 
     def trace_tuples(self):
         return [e.astuple() for e in self.bounds_trace]
@@ -338,7 +339,8 @@ def _report(r: _Report, tr, cap: int) -> DistanceReport:
         complete=bool(r.complete), upper=int(r.upper), candidates_visited=int(r.candidates_visited),
         prep_seconds=r.prep_seconds, enum_seconds=r.enum_seconds, n_gammas=r.n_gammas,
         kernel_launches=r.kernel_launches, best_generation=r.best_generation, best_gamma=r.best_gamma,
-        best_rank=int(r.best_rank), h2d_bytes=int(r.h2d_bytes), d2h_bytes=int(r.d2h_bytes))
+        best_rank=int(r.best_rank), h2d_bytes=int(r.h2d_bytes), d2h_bytes=int(r.d2h_bytes),
+        last_level_kernel=r.last_level_kernel)
 
 
 _TRACE_CAP = 512
@@ -814,6 +816,21 @@ class Comm:
         if getattr(self, "handle", None):
             library().sdb_comm_destroy(self.handle)
             self.handle = None
+
+
+def torch_allreduce_min(dist, device="cpu"):
+    """RunOptions.allreduce_min over a torch.distributed process group (gloo or nccl): the
+    host-callback form of the per-level exchange (MIN on order-preserving int64 views of the
+    uint64 values), for callers without an NCCL communicator handle (Comm)."""
+    import torch
+
+    def fn(values):
+        v = (np.asarray(values, dtype=np.uint64) ^ np.uint64(1 << 63)).view(np.int64)
+        t = torch.tensor(v, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return t.cpu().numpy().view(np.uint64) ^ np.uint64(1 << 63)
+
+    return fn
 
 
 def cli_path() -> str:

@@ -1214,6 +1214,10 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     rep->best_rank = best_r;
     rep->h2d_bytes += h2d;
     rep->d2h_bytes += d2h;
+    if (generation >= 1) {
+        const int t = levels_[size_t(generation)].t;
+        rep->last_level_kernel = t == -3 ? 3 : t == -2 ? 5 : t == -1 ? 4 : t == 0 ? 1 : 2;
+    }
     if (best_out) {
         const BitMat &m = gammas_[size_t(std::max(0, best_j))].matrix;
         std::vector<uint64_t> acc(size_t(m.stride), 0);

@@ -48,6 +48,26 @@ def test_package_routes_bit_exact(gpu, which, kernel):
             assert rep.distance == case["brute"]
 
 
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_config4_saved_2_gamma_bit_exact(gpu, kernel):
+    # the reference's saved_2_gamma on config 4 (distance.cpp:115-133; 1.5e11 candidates,
+    # 195 s on 8 threads: tests/golden/config4_s2g.json); the best codeword when its
+    # single-worker golden (config4_s2g_best.json) exists
+    gd = load_golden("config4_s2g.json")
+    c = gpu.CONFIGS[4]
+    a = gpu.generate_code(c["n"], c["k"], c["seed"])
+    rep, best = gpu.saved_2_gamma(a, gpu.RunOptions(kernel=kernel), return_best=True)
+    assert rep.distance == gd["distance"] == 10
+    assert tr(rep) == [tuple(t) for t in gd["trace"]]
+    assert rep.candidates_enumerated == rep.candidates_visited == gd["candidates"]
+    assert rep.generations == gd["generations"]
+    try:
+        gb = load_golden("config4_s2g_best.json")
+    except pytest.skip.Exception:
+        return
+    assert (best == hex_to_mat([gb["best"]], gb["best_len"])[0]).all()
+
+
 def test_auto_dispatch_sends_small_k_to_two_gamma(gpu):
     gd = load_golden("package_routes.json")["config3_auto"]
     for c in gd["codes"][:64]:

@@ -4,7 +4,7 @@ Each rank takes the product's shard of every level — lexicographic segments of
 rank space, segment s to rank s % world (csrc/engine.cpp prepare_level, kernels.cu
 walk_kernel) — scores its candidates on the CPU (the oracle's Gamma_j, the reference's
 admissibility rule engine.cpp:23-29), and merges the level minimum with the product's
-exchange: bench.make_allreduce (torch.distributed MIN on order-preserving int64 views), then
+exchange: paper_2408_10743_b200.torch_allreduce_min (torch.distributed MIN on order-preserving int64 views), then
 the key of the winning weight only (Plan::run). The merged trace and best key must equal the
 reference's single-process ones (tests/golden/config1.json).
 """
@@ -50,7 +50,7 @@ def _worker(rank: int, world: int, port: int, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         sys.path.insert(0, ROOT)
         sys.path.insert(0, os.path.join(ROOT, "tests"))
-        import bench
+        import paper_2408_10743_b200 as P
         import oracle as O
         from conftest import hex_to_mat, load_golden
 
@@ -63,7 +63,7 @@ def _worker(rank: int, world: int, port: int, q):
         filt = _rows_as_ints(a)
         mask2n = (1 << (2 * n)) - 1
         N, G = a.shape[0], len(gammas)
-        allreduce = bench.make_allreduce(torch, dist, "cpu")
+        allreduce = P.torch_allreduce_min(dist, "cpu")
         U, trace, best, visited = 3 * n + 1, [], None, 0
         for g in range(1, N + 1):
             per = len(list(itertools.combinations(range(N), g)))
