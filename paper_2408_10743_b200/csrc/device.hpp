@@ -202,6 +202,8 @@ struct TcGammaDev {
     int kc;      // the coordinate carrying -c_t on the tail side (head side -1)
     int S;       // weight scale (2: only unit-column symbols, 4: otherwise)
     int alpha;   // S / 2
+    int kt;      // threshold coordinates kt, kt + 1: tail bytes 1, 16; head bytes r, q with
+                 // 16 q + r = -(T + 1), so the accumulator is val - T - 1 (< 0 iff val <= T)
 };
 // One unit in flight. Head row r of tile a (a < na) is head rank hbase0 + r * na + a; tail
 // row y of the unit's B tiles is tail rank t0 + (y % 256) * nbt + y / 256 (each producer
@@ -212,8 +214,18 @@ struct TcUnitDesc {
     int j, b, nheads, ntails, nbt, na, bb, restage, end, pad;
 };
 struct TcSlotMeta {
-    short ch[kTcHeads];  // per head row: alpha * |S_h ∩ mask rows|
+    short ch[kTcHeads];    // per head row: alpha * |S_h ∩ mask rows|
+    short tenc[kTcHeads];  // per head row: the threshold T folded into its kt bytes
 };
+// -(T + 1) as the head's two threshold bytes (r at kt, q at kt + 1; the tail holds 1, 16),
+// clamped to what they can carry: a larger T only sends more pairs down the exact path, a
+// T below -2048 passes nothing either way (|val| <= 2 K)
+SDB_HD inline void tc_threshold_bytes(int T, int &r, int &q) {
+    int m = -(T + 1);
+    m = m < -2048 ? -2048 : m > 2047 ? 2047 : m;
+    q = m >> 4;  // floor division: -2048 .. 2047 -> -128 .. 127
+    r = m & 15;
+}
 struct TcPlan {
     TilePlan tile;            // unit table over head blocks of kTcHeads * kTcUnitTiles, tchunk = kTcTileN * nbt
     int nbt;                  // B tiles per unit

@@ -75,13 +75,16 @@ __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Waits for the phase with the given parity to complete. The suspend-time hint lets the
+// hardware park the warp until the phase flips (instead of re-issuing the test), so waiting
+// warps leave the issue slots to the working ones.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
 }
 
@@ -119,6 +122,13 @@ __device__ __forceinline__ void ld16_pack(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 __device__ __forceinline__ int min3i(int a, int b, int c) { return min(min(a, b), c); }
+
+// a | b | c as one LOP3 that ptxas keeps where it stands (no re-association into chains)
+__device__ __forceinline__ uint32_t or3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xFE;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
 
 }  // namespace tc
 }  // namespace sdb

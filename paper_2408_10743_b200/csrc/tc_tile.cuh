@@ -144,6 +144,8 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
             if (cc >= 0) tile[tc::kmajor_off(kTcTileN, trow, cc)] = 0;
         }
         tile[tc::kmajor_off(kTcTileN, trow, gm.kc)] = (unsigned char)(-(gm.alpha * cnt));
+        tile[tc::kmajor_off(kTcTileN, trow, gm.kt)] = 1;
+        tile[tc::kmajor_off(kTcTileN, trow, gm.kt + 1)] = 16;
     }
 }
 
@@ -152,7 +154,8 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
 template <int H, int KW>
 __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, int pt, int lane, int c0, int kmax,
                               const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
-                              unsigned char *sA, TcSlotMeta *s_meta, TcShared &sh) {
+                              unsigned char *sA, TcSlotMeta *s_meta, TcShared &sh, const unsigned *s_thr,
+                              unsigned sshift) {
     const int r0 = pt * d.na;
     int e[kTcMaxPart];
     int a = (g - c0) & 1;  // first tile of this group
@@ -180,13 +183,57 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
             const int cc = mk[e[k]];
             if (cc >= 0) tile[tc::kmajor_off(kTcHeads, pt, cc)] = 0;
         }
-        s_meta[s].ch[pt] = short(gm.alpha * cnt);
+        // the threshold, folded into the MMA: the accumulator of a pair is val - T - 1 (T from
+        // the CTA's current bound; rows past the unit's heads never pass)
+        const int chv = gm.alpha * cnt;
+        const int T = r0 + a < d.nheads ? gm.S * int(*(volatile const unsigned *)s_thr >> sshift) - gm.C0 - chv
+                                        : -32768;
+        int tr = 0, tq = 0;
+        tc_threshold_bytes(T, tr, tq);
+        tile[tc::kmajor_off(kTcHeads, pt, gm.kt)] = (unsigned char)tr;
+        tile[tc::kmajor_off(kTcHeads, pt, gm.kt + 1)] = (unsigned char)tq;
+        s_meta[s].ch[pt] = short(chv);
+        s_meta[s].tenc[pt] = short(T);
         tc::fence_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sh.afull[s]);
         wrote++;
     }
     return wrote;
+}
+
+#ifdef SDB_TC_PROF
+#define TCP_ARGS , tcp_t0, tcp_acc
+#define TCP_PARAMS , unsigned long long &tcp_t0, unsigned long long (&tcp_acc)[8]
+#else
+#define TCP_ARGS
+#define TCP_PARAMS
+#endif
+
+// The MMA thread's inner loop: one head tile (descriptor aT) against the unit's nbt tail tiles,
+// one TMEM stage each. Kept lean: the tensor pipe takes about one MMA ahead, so every cycle
+// the issuer spends between MMAs is a bubble.
+template <int KT>
+__device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t b_tile16, int nbt, uint32_t tbase,
+                                              uint32_t idesc, uint32_t &st, uint32_t &tpar, TcShared &sh TCP_PARAMS) {
+    for (int nb = 0; nb < nbt; nb++) {
+        TCP_BEGIN
+        tc::mbar_wait(&sh.tempty[st], tpar ^ 1);
+        TCP_END(3)
+        TCP_BEGIN
+        tc::fence_after();
+        const uint64_t bT = bU + uint64_t(nb) * b_tile16;
+#ifndef SDB_TC_NOMMA  // pipeline experiments: the MMAs skipped
+#pragma unroll
+        for (int k = 0; k < KT; k++)
+            tc::mma_i8(tbase + st * kTcTileN, aT + uint64_t(k * 2 * kTcHeads), bT + uint64_t(k * 2 * kTcTileN), idesc,
+                       k > 0);
+#endif
+        tc::commit(&sh.tfull[st]);
+        TCP_END(4)
+        st ^= 1u;
+        tpar ^= st == 0 ? 1u : 0u;
+    }
 }
 
 template <int W, int KW>
@@ -196,6 +243,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     __shared__ TcShared sh;
     __shared__ uint32_t s_tbase;
     __shared__ unsigned long long s_visited;
+    __shared__ unsigned s_thr;  // the CTA's bound (scaled weight units): producers fold it into head rows
     const TilePlan &tl = tp.tile;
     const int G = p.G, N = p.N, kmax = tp.kmax;
     const int BKs = min(p.BK, tl.g + 2);
@@ -237,6 +285,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         }
         tc::mbar_fence_init();
         s_visited = 0;
+        s_thr = start_threshold(p, tl.thr0);
     }
     if (warp == 0) tc::tmem_alloc(&s_tbase, 512);
     tc::fence_before();
@@ -250,8 +299,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_i8(kTcHeads, kTcTileN);
-            const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB);
+            // operand descriptors; an offset of x bytes is + (x >> 4) on the start-address field
+            const uint64_t aD = tc::sdesc(tc::smem_u32(sA), kTcHeads * 16, 128);
+            const uint64_t bD = tc::sdesc(tc::smem_u32(sB), kTcTileN * 16, 128);
+            const uint32_t b_tile16 = uint32_t((size_t(kTcTileN) * kmax) >> 4);
             int ts = 0, cur_bb = -1;
+            uint32_t st = 0, tpar = 0;  // next TMEM stage and the parity its tempty wait expects
             int uses[2] = {0, 0}, c = 0;
             TCP_DECL
             const unsigned long long tcp_start = clock64();
@@ -263,7 +316,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
                 if (d.end) {
 #ifdef SDB_TC_PROF
-                    if (blockIdx.x == 0) printf("[tcprof] mma: total %llu wait_uq %llu wait_bfull %llu wait_afull %llu wait_tempty %llu stages %d\n", clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3], ts);
+                    if (blockIdx.x == 0) printf("[tcprof] mma: total %llu wait_uq %llu wait_bfull %llu wait_afull %llu wait_tempty %llu issue %llu stages %d\n", clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3], tcp_acc[4], ts);
 #endif
                     break;
                 }
@@ -276,27 +329,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     uses[cur_bb]++;
                 }
                 const int KT = s_gam[d.j].K / 32;
+                const uint64_t bU = bD + uint64_t((size_t(cur_bb) * b_buf) >> 4);
                 for (int a = 0; a < d.na; a++, c++) {
                     const int s = tc_slot(c);
                     TCP_BEGIN
                     tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
                     TCP_END(2)
                     tc::fence_after();
-                    const uint32_t a0 = aBase + uint32_t(s * a_slot);
-                    for (int nb = 0; nb < d.nbt; nb++, ts++) {
-                        const int st = ts % kTcStages;
-                        TCP_BEGIN
-                        tc::mbar_wait(&sh.tempty[st], ((ts / kTcStages) & 1) ^ 1);
-                        TCP_END(3)
-                        tc::fence_after();
-                        const uint32_t b0 = bBase + uint32_t(cur_bb * b_buf + size_t(nb) * kTcTileN * kmax);
-                        for (int k = 0; k < KT; k++) {
-                            const uint64_t ad = tc::sdesc(a0 + k * 2 * (kTcHeads * 16), kTcHeads * 16, 128);
-                            const uint64_t bd = tc::sdesc(b0 + k * 2 * (kTcTileN * 16), kTcTileN * 16, 128);
-                            tc::mma_i8(tbase + st * kTcTileN, ad, bd, idesc, k > 0);
-                        }
-                        tc::commit(&sh.tfull[st]);
+                    const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
+                    switch (KT) {
+                        case 1: tc_mma_stages<1>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
+                        case 2: tc_mma_stages<2>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
+                        case 3: tc_mma_stages<3>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
+                        default: tc_mma_stages<4>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
                     }
+                    ts += d.nbt;
                     tc::commit(&sh.aempty[s]);
                 }
             }
@@ -308,6 +355,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const int row = 32 * q + lane;      // head row of the tile = TMEM lane
         const unsigned sshift = p.scale == 2 ? 1u : 0u;
         unsigned thrH = start_threshold(p, tl.thr0);
+        unsigned s_thr_seen = thrH;  // this warp's last bound published to s_thr
         int ts = 0;
         int c = 0;  // head tiles consumed
         TCP_DECL
@@ -338,12 +386,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 TCP_BEGIN
                 tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
                 TCP_END(1)
-                const int ch = s_meta[s].ch[row];
+                const int ch = s_meta[s].ch[row], tenc = s_meta[s].tenc[row];
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sh.aempty[s]);
                 const int hoff = row * d.na + a;  // this row's head: rank hbase0 + hoff
-                // other CTAs' finds tighten the threshold from the next tile on (the load's
-                // latency overlaps this tile's stages)
+                // other CTAs' finds tighten the bound from the next tile on (the load's latency
+                // overlaps this tile's stages)
                 const unsigned wmin_seen = *(volatile unsigned int *)&p.state->wmin;
                 int T = hoff < d.nheads ? gm.S * int(thrH >> sshift) - gm.C0 - ch : -32768;
                 for (int nb = 0; nb < d.nbt; nb++, ts++) {
@@ -360,18 +408,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     tc::ld16_pack(ta + 64, v[2]);
                     tc::ld16_pack(ta + 96, v[3]);
                     tc::ld_wait();
-                    // tree of packed minimums (short dependency chains)
-                    uint32_t m8[16];
+                    // a pair passes the folded threshold iff its 16-bit accumulator is negative:
+                    // OR the packed words, test the two sign bits
+                    // as a tree of 3-input ORs (depth 4): ptxas turns a plain OR reduction into
+                    // one 32-deep dependent LOP3 chain, which sets the epilogue's latency
+                    uint32_t r[22];
 #pragma unroll
-                    for (int i = 0; i < 16; i++) m8[i] = __vmins2(__vmins2(v[0][i], v[1][i]), __vmins2(v[2][i], v[3][i]));
+                    for (int i = 0; i < 21; i++) r[i] = tc::or3(v[(3 * i) >> 4][(3 * i) & 15], v[(3 * i + 1) >> 4][(3 * i + 1) & 15],
+                                                                v[(3 * i + 2) >> 4][(3 * i + 2) & 15]);
+                    r[21] = v[3][15];
+                    uint32_t r2[8];
 #pragma unroll
-                    for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-                        for (int i = 0; i < w; i++) m8[i] = __vmins2(m8[i], m8[i + w]);
-                    const uint32_t mn = m8[0];
-                    const int lo = int(short(mn & 0xFFFFu)), hi = int(short(mn >> 16));
-                    if (min(lo, hi) <= T) {
-                        // rare: the exact path for every pair at or below the threshold
+                    for (int i = 0; i < 7; i++) r2[i] = tc::or3(r[3 * i], r[3 * i + 1], r[3 * i + 2]);
+                    r2[7] = r[21];
+                    const uint32_t o = tc::or3(tc::or3(r2[0], r2[1], r2[2]), tc::or3(r2[3], r2[4], r2[5]), r2[6] | r2[7]);
+#if defined(SDB_TC_NOMMA) || defined(SDB_TC_NOPROD)
+                    o = 0;  // TMEM / the operands hold no real data
+#endif
+                    if (o & 0x80008000u) {
+                        // rare: the exact path for every pair below the folded threshold that
+                        // also passes the current one (val = acc + tenc + 1 <= T)
                         uint32_t all[64];
 #pragma unroll
                         for (int i = 0; i < 16; i++) {
@@ -381,8 +437,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                             all[48 + i] = v[3][i];
                         }
                         for (int x = 0; x < 128; x++) {
-                            const int val = int(short(all[x >> 1] >> (16 * (x & 1))));
-                            if (val > T) continue;
+                            const int acc = int(short(all[x >> 1] >> (16 * (x & 1))));
+                            if (acc >= 0 || acc + tenc + 1 > T) continue;
                             const int y = nb * kTcTileN + half * 128 + x;  // B row of the unit
                             const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
                                                 d.ntails - 1);
@@ -396,6 +452,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     TCP_END(3)
                 }
                 thrH = min(thrH, wmin_seen);
+                // hand a tighter bound to the producers' next head tiles (s_thr_seen is
+                // warp-uniform; the loop above is too, so the whole warp gets here)
+                if (__any_sync(0xffffffffu, thrH < s_thr_seen)) {
+                    const unsigned m = __reduce_min_sync(0xffffffffu, thrH);
+                    if (lane == 0) atomicMin(&s_thr, m);
+                    s_thr_seen = m;
+                }
             }
         }
     } else if (warp == kTcEpiWarps + 1) {
@@ -457,6 +520,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         }
     } else {
         // ------------------------------------------------------------ producers
+        const unsigned sshift = p.scale == 2 ? 1u : 0u;
         const int pw = warp - (kTcEpiWarps + 2);   // 0..7
         const int g = pw >> 2;                     // group: head tiles c with c % 2 == g
         const int pt = 32 * (pw & 3) + lane;       // head row
@@ -478,6 +542,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 fills[bb]++;
                 __syncwarp();
                 unsigned char *buf = sB + size_t(bb) * b_buf;
+#ifndef SDB_TC_NOPROD  // pipeline experiments: the producers only signal
                 switch (tl.t - 1) {
 #define SDB_TC_TAILS(m) \
     case m: tc_write_tails<m, KW>(d, gm, pq, N, kmax, sg, mk, s_binom, BKs, buf); break;
@@ -485,17 +550,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     SDB_TC_TAILS(5) SDB_TC_TAILS(6) SDB_TC_TAILS(7) SDB_TC_TAILS(8)
 #undef SDB_TC_TAILS
                 }
+#endif
                 tc::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sh.bfull[bb]);
             }
+#ifdef SDB_TC_NOPROD
+            for (int a = (g - c0) & 1; a < d.na; a += 2) {
+                const int s = tc_slot(c0 + a);
+                if (lane == 0) tc::mbar_wait(&sh.aempty[s], tc_slot_par(c0 + a) ^ 1);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sh.afull[s]);
+            }
+#else
             switch (tl.h) {
 #define SDB_TC_HEADS(m) \
-    case m: tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, sh); break;
+    case m:                                                                                                \
+        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, sh, &s_thr, sshift); \
+        break;
                 SDB_TC_HEADS(1) SDB_TC_HEADS(2) SDB_TC_HEADS(3) SDB_TC_HEADS(4)
                 SDB_TC_HEADS(5) SDB_TC_HEADS(6) SDB_TC_HEADS(7) SDB_TC_HEADS(8)
 #undef SDB_TC_HEADS
             }
+#endif
             c0 += d.na;
         }
     }

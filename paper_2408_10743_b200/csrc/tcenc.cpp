@@ -127,6 +127,9 @@ TcEncoding tc_encode(const std::vector<const BitMat *> &mats, int N, int n, bool
         }
         gm.kc = int(L.size());
         L.push_back(Coord{-1, -1, -1});
+        gm.kt = int(L.size());  // two threshold coordinates (not padding: they carry -(T + 1))
+        L.push_back(Coord{-1, -1, -1});
+        L.push_back(Coord{-1, -1, -1});
         while (L.size() % 32) {
             L.push_back(Coord{-1, -1, -1});
             pad_v += 1;
@@ -198,13 +201,26 @@ int tc_selfcheck(const TcEncoding &enc, const std::vector<const BitMat *> &mats,
                     if (c >= 0) v[size_t(c)] = 0;
                 }
                 if (!is_head) v[size_t(gm.kc)] = int8_t(-(gm.alpha * cnt));
+                v[size_t(gm.kt)] = v[size_t(gm.kt + 1)] = 0;
                 return v;
             };
             int ch = 0, ct = 0;
-            const std::vector<int8_t> hv = bytes(head, true, ch), tv = bytes(tail, false, ct);
+            std::vector<int8_t> hv = bytes(head, true, ch), tv = bytes(tail, false, ct);
             int acc = 0;
             for (int k = 0; k < gm.K; k++) acc += int(hv[size_t(k)]) * int(tv[size_t(k)]);
             if (gm.S * w != gm.C0 + gm.alpha * ch + acc) bad++;
+            // the threshold fold: with T = S thr - C0 - ch in the head's kt bytes and 1, 16 in
+            // the tail's, the accumulator is negative iff w <= thr
+            const int thr = w + int(rng() % 5) - 2;
+            int r = 0, q = 0;
+            tc_threshold_bytes(gm.S * thr - gm.C0 - gm.alpha * ch, r, q);
+            hv[size_t(gm.kt)] = int8_t(r);
+            hv[size_t(gm.kt + 1)] = int8_t(q);
+            tv[size_t(gm.kt)] = 1;
+            tv[size_t(gm.kt + 1)] = 16;
+            int acc2 = 0;
+            for (int k = 0; k < gm.K; k++) acc2 += int(hv[size_t(k)]) * int(tv[size_t(k)]);
+            if ((acc2 < 0) != (w <= thr) || int(int16_t(acc2)) != acc2) bad++;
         }
     }
     (void)image;

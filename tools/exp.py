@@ -38,7 +38,7 @@ def ms(xs):
 
 def cmd_time(a):
     for cid in a.configs:
-        gmax = a.gmax if cid == 5 else 0
+        gmax = a.gmax if cid == 5 or a.gmax != 9 else 0
         with P.Plan(code(cid), P.RunOptions(kernel=a.kernel, max_generation=gmax)) as pl:
             pl.run()
             r = pl.run()
