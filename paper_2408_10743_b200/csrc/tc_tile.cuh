@@ -213,6 +213,13 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
 // The MMA thread's inner loop: one head tile (descriptor aT) against the unit's nbt tail tiles,
 // one TMEM stage each. Kept lean: the tensor pipe takes about one MMA ahead, so every cycle
 // the issuer spends between MMAs is a bubble.
+// a relaxed (not .sys) load of a word other CTAs update with atomics
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <int KT>
 __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t b_tile16, int nbt, uint32_t tbase,
                                               uint32_t idesc, uint32_t &st, uint32_t &tpar, TcShared &sh TCP_PARAMS) {
@@ -226,10 +233,10 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t
 #ifndef SDB_TC_NOMMA  // pipeline experiments: the MMAs skipped
 #pragma unroll
         for (int k = 0; k < KT; k++)
-            tc::mma_i8(tbase + st * kTcTileN, aT + uint64_t(k * 2 * kTcHeads), bT + uint64_t(k * 2 * kTcTileN), idesc,
-                       k > 0);
+            tc::mma_i8_elect(tbase + st * kTcTileN, aT + uint64_t(k * 2 * kTcHeads), bT + uint64_t(k * 2 * kTcTileN),
+                             idesc, k > 0);
 #endif
-        tc::commit(&sh.tfull[st]);
+        tc::commit_elect(&sh.tfull[st]);
         TCP_END(4)
         st ^= 1u;
         tpar ^= st == 0 ? 1u : 0u;
@@ -273,7 +280,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         }
         for (int s = 0; s < kTcSlots; s++) {
             tc::mbar_init(&sh.afull[s], kTcProdWarps / 2);   // the four warps of the writing group
+#ifdef SDB_TC_EPI_NOMETA
+            tc::mbar_init(&sh.aempty[s], 1);
+#else
             tc::mbar_init(&sh.aempty[s], 1 + kTcEpiWarps);   // MMA commit + epilogue (read the slot's meta)
+#endif
         }
         for (int s = 0; s < 2; s++) {
             tc::mbar_init(&sh.bfull[s], kTcProdWarps);
@@ -296,8 +307,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     const size_t b_buf = size_t(tp.nbt) * kTcTileN * kmax;   // bytes per tail buffer
 
     if (warp == 0) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // ------------------------------------------------------------ MMA issuer: the whole
+        // warp runs the loop converged (warp-uniform values stay in uniform registers); one
+        // elected lane issues each tcgen05.mma / commit (tc::mma_i8_elect, tc::commit_elect)
+        {
             const uint32_t idesc = tc::idesc_i8(kTcHeads, kTcTileN);
             // operand descriptors; an offset of x bytes is + (x >> 4) on the start-address field
             const uint64_t aD = tc::sdesc(tc::smem_u32(sA), kTcHeads * 16, 128);
@@ -313,15 +326,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
                 TCP_END(0)
                 const TcUnitDesc d = s_uq[u % kTcUnitQ];
-                tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
                 if (d.end) {
 #ifdef SDB_TC_PROF
-                    if (blockIdx.x == 0) printf("[tcprof] mma: total %llu wait_uq %llu wait_bfull %llu wait_afull %llu wait_tempty %llu issue %llu stages %d\n", clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3], tcp_acc[4], ts);
+                    if (blockIdx.x == 0 && lane == 0) printf("[tcprof] mma: total %llu wait_uq %llu wait_bfull %llu wait_afull %llu wait_tempty %llu issue %llu stages %d\n", clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3], tcp_acc[4], ts);
 #endif
                     break;
                 }
                 if (d.restage) {
-                    if (cur_bb >= 0) tc::commit(&sh.bempty[cur_bb]);  // old buffer free once its MMAs finish
+                    if (cur_bb >= 0) tc::commit_elect(&sh.bempty[cur_bb]);  // old buffer free once its MMAs finish
                     cur_bb = d.bb;
                     TCP_BEGIN
                     tc::mbar_wait(&sh.bfull[cur_bb], uses[cur_bb] & 1);
@@ -332,9 +346,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 const uint64_t bU = bD + uint64_t((size_t(cur_bb) * b_buf) >> 4);
                 for (int a = 0; a < d.na; a++, c++) {
                     const int s = tc_slot(c);
+#ifndef SDB_TC_MMA_NOAFULL
                     TCP_BEGIN
                     tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
                     TCP_END(2)
+#endif
                     tc::fence_after();
                     const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
                     switch (KT) {
@@ -344,7 +360,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                         default: tc_mma_stages<4>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
                     }
                     ts += d.nbt;
-                    tc::commit(&sh.aempty[s]);
+                    tc::commit_elect(&sh.aempty[s]);
                 }
             }
         }
@@ -356,6 +372,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const unsigned sshift = p.scale == 2 ? 1u : 0u;
         unsigned thrH = start_threshold(p, tl.thr0);
         unsigned s_thr_seen = thrH;  // this warp's last bound published to s_thr
+        unsigned wmin_next = thrH;   // the level minimum as loaded at the previous head tile
         int ts = 0;
         int c = 0;  // head tiles consumed
         TCP_DECL
@@ -383,16 +400,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             un.pad = d.nheads;
             for (int a = 0; a < d.na; a++, c++) {
                 const int s = tc_slot(c);
+#ifdef SDB_TC_EPI_NOMETA
+                const int ch = 0, tenc = 0;
+#else
                 TCP_BEGIN
                 tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
                 TCP_END(1)
                 const int ch = s_meta[s].ch[row], tenc = s_meta[s].tenc[row];
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sh.aempty[s]);
+#endif
                 const int hoff = row * d.na + a;  // this row's head: rank hbase0 + hoff
-                // other CTAs' finds tighten the bound from the next tile on (the load's latency
-                // overlaps this tile's stages)
-                const unsigned wmin_seen = *(volatile unsigned int *)&p.state->wmin;
+                // other CTAs' finds: the value loaded one head tile ago (its L2 latency hidden
+                // behind that tile's stages) tightens the bound now; load the next one
+                thrH = min(thrH, wmin_next);
+                wmin_next = ld_relaxed_u32(&p.state->wmin);
                 int T = hoff < d.nheads ? gm.S * int(thrH >> sshift) - gm.C0 - ch : -32768;
                 for (int nb = 0; nb < d.nbt; nb++, ts++) {
                     const int st = ts % kTcStages;
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #pragma unroll
                     for (int i = 0; i < 7; i++) r2[i] = tc::or3(r[3 * i], r[3 * i + 1], r[3 * i + 2]);
                     r2[7] = r[21];
-                    const uint32_t o = tc::or3(tc::or3(r2[0], r2[1], r2[2]), tc::or3(r2[3], r2[4], r2[5]), r2[6] | r2[7]);
+                    uint32_t o = tc::or3(tc::or3(r2[0], r2[1], r2[2]), tc::or3(r2[3], r2[4], r2[5]), r2[6] | r2[7]);
 #if defined(SDB_TC_NOMMA) || defined(SDB_TC_NOPROD)
                     o = 0;  // TMEM / the operands hold no real data
 #endif
@@ -451,7 +473,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     if (lane == 0) tc::mbar_arrive(&sh.tempty[st]);
                     TCP_END(3)
                 }
-                thrH = min(thrH, wmin_seen);
                 // hand a tighter bound to the producers' next head tiles (s_thr_seen is
                 // warp-uniform; the loop above is too, so the whole warp gets here)
                 if (__any_sync(0xffffffffu, thrH < s_thr_seen)) {

@@ -31,7 +31,7 @@ constexpr int M = 128, NB = 256;  // B holds 256 rows; a stage uses N of them
 
 __device__ __forceinline__ uint32_t idesc(int n) { return idesc_i8(M, n); }
 
-template <int KT, int NS, int N, int E, int GROUPS, int EPI>
+template <int KT, int NS, int N, int E, int GROUPS, int EPI, int NA = 1, int NBT = 1>
 __global__ void __launch_bounds__(32 * (1 + E), 1) pipe_bench(int T, long long *cycles, int *out) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t full[NS], empty[NS];
@@ -41,10 +41,10 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) pipe_bench(int T, long long *
     constexpr int QW = WPS / 4;              // warps per lane quarter and stage
     constexpr int COLS = N / QW;             // columns per warp and stage
     static_assert(COLS % 32 == 0, "a warp reads whole 32-column chunks");
-    unsigned char *sA = sm, *sB = sm + M * KB;
+    unsigned char *sA = sm, *sB = sm + NA * M * KB;  // NA A tiles, NBT B tiles (rotated like the kernel)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) tmem_alloc(&tbase, 512);
-    for (int i = threadIdx.x; i < (M + NB) * KB; i += blockDim.x) sm[i] = (unsigned char)((i * 7 + 3) % 5 - 2);
+    for (int i = threadIdx.x; i < (NA * M + NBT * NB) * KB; i += blockDim.x) sm[i] = (unsigned char)((i * 7 + 3) % 5 - 2);
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; s++) {
             mbar_init(&full[s], 1);
@@ -69,10 +69,11 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) pipe_bench(int T, long long *
                 mbar_wait(&empty[s], ph ^ 1);
                 fence_after();
                 const int boff = (it % (NB / N)) * N;  // which N rows of B
+                const int ta_ = (it / NBT) % NA, tb_ = it % NBT;  // like the kernel: a head tile meets NBT tail tiles
 #pragma unroll
                 for (int k = 0; k < KT; k++) {
-                    const uint64_t ad = sdesc(smem_u32(sA) + k * 2 * (M * 16), M * 16, 128);
-                    const uint64_t bd = sdesc(smem_u32(sB) + boff * 16 + k * 2 * (NB * 16), NB * 16, 128);
+                    const uint64_t ad = sdesc(smem_u32(sA) + ta_ * M * KB + k * 2 * (M * 16), M * 16, 128);
+                    const uint64_t bd = sdesc(smem_u32(sB) + tb_ * NB * KB + boff * 16 + k * 2 * (NB * 16), NB * 16, 128);
                     mma_i8(tb + s * N, ad, bd, id, k > 0);
                 }
                 commit(&full[s]);
@@ -120,11 +121,11 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) pipe_bench(int T, long long *
     if (warp == 0) tmem_dealloc(tb, 512);
 }
 
-template <int KT, int NS, int N, int E, int GROUPS, int EPI>
+template <int KT, int NS, int N, int E, int GROUPS, int EPI, int NA = 1, int NBT = 1>
 void run(int T, int nsm, long long *dcyc, int *dout) {
     constexpr int KB = 32 * KT;
-    const size_t smem = size_t(M + NB) * KB;
-    auto kern = pipe_bench<KT, NS, N, E, GROUPS, EPI>;
+    const size_t smem = size_t(NA * M + NBT * NB) * KB;
+    auto kern = pipe_bench<KT, NS, N, E, GROUPS, EPI, NA, NBT>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<nsm, 32 * (1 + E), smem>>>(16, dcyc, dout);
     CK(cudaDeviceSynchronize());
@@ -135,7 +136,7 @@ void run(int T, int nsm, long long *dcyc, int *dout) {
     double avg = 0;
     for (long long c : cyc) avg += double(c);
     avg /= nsm;
-    printf("KT=%d NS=%d N=%3d E=%2d groups=%d epi=%-6s: %7.1f cyc per 128x256 tile, %6.1f cand/clk/SM (MMA floor %d)\n", KT,
+    printf("NA=%d NBT=%d KT=%d NS=%d N=%3d E=%2d groups=%d epi=%-6s: %7.1f cyc per 128x256 tile, %6.1f cand/clk/SM (MMA floor %d)\n", NA, NBT, KT,
            NS, N, E, GROUPS, EPI == 0 ? "min16" : EPI == 1 ? "or16" : "ld", avg / T, double(M) * NB * T / avg, 128 * KT);
 }
 
@@ -149,31 +150,13 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&dcyc, nsm * 8));
     CK(cudaMalloc(&dout, nsm * 4));
     printf("device %s, %d SMs, T=%d tiles per SM\n", prop.name, nsm, T);
-    // today's shape
-    run<2, 2, 256, 8, 1, 0>(T, nsm, dcyc, dout);
     run<2, 2, 256, 8, 1, 1>(T, nsm, dcyc, dout);
-    run<2, 2, 256, 8, 1, 2>(T, nsm, dcyc, dout);
-    run<2, 2, 256, 8, 2, 0>(T, nsm, dcyc, dout);
-    run<2, 2, 256, 8, 2, 1>(T, nsm, dcyc, dout);
-    run<2, 2, 256, 16, 2, 1>(T, nsm, dcyc, dout);
-    // more, smaller stages
-    run<2, 4, 128, 8, 1, 0>(T, nsm, dcyc, dout);
-    run<2, 4, 128, 8, 1, 1>(T, nsm, dcyc, dout);
-    run<2, 4, 128, 8, 2, 0>(T, nsm, dcyc, dout);
-    run<2, 4, 128, 8, 2, 1>(T, nsm, dcyc, dout);
-    run<2, 4, 128, 16, 2, 1>(T, nsm, dcyc, dout);
-    run<2, 4, 128, 16, 4, 1>(T, nsm, dcyc, dout);
-    run<2, 4, 128, 8, 1, 2>(T, nsm, dcyc, dout);
-    run<2, 8, 64, 8, 1, 1>(T, nsm, dcyc, dout);
-    run<2, 8, 64, 8, 2, 1>(T, nsm, dcyc, dout);
-    run<2, 8, 64, 16, 4, 1>(T, nsm, dcyc, dout);
-    // K = 96 and 128
-    run<3, 2, 256, 8, 1, 0>(T, nsm, dcyc, dout);
-    run<3, 4, 128, 8, 2, 1>(T, nsm, dcyc, dout);
-    run<3, 4, 128, 16, 4, 1>(T, nsm, dcyc, dout);
-    run<4, 4, 128, 8, 2, 1>(T, nsm, dcyc, dout);
-    run<4, 4, 128, 16, 4, 1>(T, nsm, dcyc, dout);
-    // MMA only (the epilogue hands stages straight back)
+    run<2, 2, 256, 8, 1, 1, 4, 1>(T, nsm, dcyc, dout);
+    run<2, 2, 256, 8, 1, 1, 1, 5>(T, nsm, dcyc, dout);
+    run<2, 2, 256, 8, 1, 1, 4, 5>(T, nsm, dcyc, dout);
+    run<2, 2, 256, 8, 1, 2, 4, 5>(T, nsm, dcyc, dout);
+    run<3, 2, 256, 8, 1, 1, 1, 1>(T, nsm, dcyc, dout);
+    run<3, 2, 256, 8, 1, 1, 4, 3>(T, nsm, dcyc, dout);
     printf("done\n");
     return 0;
 }
