@@ -184,7 +184,10 @@ int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int
 // a pair at or below the row's threshold takes the exact rare path (tile_exact), so results
 // are bit-identical to the POPC kernels.
 constexpr int kTcHeads = 128;      // heads per head tile (MMA M)
-constexpr int kTcUnitTiles = 8;    // head tiles per unit: a unit holds up to 1024 heads
+#ifndef SDB_TC_UNIT_TILES
+#define SDB_TC_UNIT_TILES 16
+#endif
+constexpr int kTcUnitTiles = SDB_TC_UNIT_TILES;  // head tiles per unit (a unit holds up to 128 x this many heads)
 constexpr int kTcMaxPart = 8;      // h <= 8 and t - 1 <= 8 (element lists live in registers)
 constexpr int kTcTileN = 256;      // tails per B tile = MMA N = TMEM columns per stage
 constexpr int kTcStages = 2;       // TMEM stages (512 columns)

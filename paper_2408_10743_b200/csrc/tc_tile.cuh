@@ -117,6 +117,23 @@ struct TcShared {
     uint64_t uqfull[kTcUnitQ], uqempty[kTcUnitQ], afull[kTcSlots], aempty[kTcSlots], bfull[2], bempty[2],
         tfull[kTcStages], tempty[kTcStages];
 };
+// shared-window addresses of the mbarrier arrays (bar i of an array at base + 8 i), computed
+// once per thread
+struct TcBars {
+    uint32_t uqfull, uqempty, afull, aempty, bfull, bempty, tfull, tempty;
+    __device__ explicit TcBars(TcShared &sh) {
+        const uint32_t b = tc::smem_u32(&sh);
+        uqfull = b + uint32_t(offsetof(TcShared, uqfull));
+        uqempty = b + uint32_t(offsetof(TcShared, uqempty));
+        afull = b + uint32_t(offsetof(TcShared, afull));
+        aempty = b + uint32_t(offsetof(TcShared, aempty));
+        bfull = b + uint32_t(offsetof(TcShared, bfull));
+        bempty = b + uint32_t(offsetof(TcShared, bempty));
+        tfull = b + uint32_t(offsetof(TcShared, tfull));
+        tempty = b + uint32_t(offsetof(TcShared, tempty));
+    }
+};
+__device__ __forceinline__ uint32_t bar_at(uint32_t base, int i) { return base + 8u * uint32_t(i); }
 
 // Producer thread pq (0..255): this unit's tails pq * nbt .. + nbt - 1 into B rows r * 256 + pq.
 template <int T1, int KW>
@@ -154,7 +171,7 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
 template <int H, int KW>
 __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, int pt, int lane, int c0, int kmax,
                               const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
-                              unsigned char *sA, TcSlotMeta *s_meta, TcShared &sh, const unsigned *s_thr,
+                              unsigned char *sA, TcSlotMeta *s_meta, const TcBars &bars, const unsigned *s_thr,
                               unsigned sshift) {
     const int r0 = pt * d.na;
     int e[kTcMaxPart];
@@ -172,7 +189,7 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
         int cnt;
         tc_gather<H, KW, false>(sg, mk, 0, 0, e, sw, cnt);
         const int c = c0 + a, s = tc_slot(c);
-        if (lane == 0) tc::mbar_wait(&sh.aempty[s], tc_slot_par(c) ^ 1);
+        if (lane == 0) tc::mbar_wait_a(bar_at(bars.aempty, s), tc_slot_par(c) ^ 1);
         __syncwarp();
         unsigned char *tile = sA + size_t(s) * a_slot;
 #pragma unroll
@@ -196,7 +213,7 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
         s_meta[s].tenc[pt] = short(T);
         tc::fence_async_smem();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&sh.afull[s]);
+        if (lane == 0) tc::mbar_arrive_a(bar_at(bars.afull, s));
         wrote++;
     }
     return wrote;
@@ -220,13 +237,41 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
     return v;
 }
 
+#ifdef SDB_TC_GAPS
+// stage-to-stage issue gaps of the MMA warp, by boundary kind: 0 inside a head tile, 1 first
+// stage of a head tile, 2 first stage of a unit (block 0 prints them)
+struct TcGaps {
+    unsigned long long last = 0, sum[3] = {0, 0, 0}, n[3] = {0, 0, 0}, wait[3] = {0, 0, 0}, afw = 0, uqw = 0;
+};
+#define TCG_PARAMS , TcGaps &gp, int kind0
+#define TCG_ARGS(k) , gaps, (k)
+#else
+#define TCG_PARAMS
+#define TCG_ARGS(k)
+#endif
+
 template <int KT>
 __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t b_tile16, int nbt, uint32_t tbase,
-                                              uint32_t idesc, uint32_t &st, uint32_t &tpar, TcShared &sh TCP_PARAMS) {
+                                              uint32_t idesc, uint32_t &st, uint32_t &tpar, const TcBars &bars TCP_PARAMS TCG_PARAMS) {
     for (int nb = 0; nb < nbt; nb++) {
+#ifdef SDB_TC_GAPS
+        const unsigned long long w0 = clock64();
+#endif
         TCP_BEGIN
-        tc::mbar_wait(&sh.tempty[st], tpar ^ 1);
+        tc::mbar_wait_a(bar_at(bars.tempty, st), tpar ^ 1);
         TCP_END(3)
+#ifdef SDB_TC_GAPS
+        {
+            const unsigned long long now = clock64();
+            const int kind = nb == 0 ? kind0 : 0;
+            if (gp.last) {
+                gp.sum[kind] += now - gp.last;
+                gp.wait[kind] += now - w0;
+                gp.n[kind]++;
+            }
+            gp.last = now;
+        }
+#endif
         TCP_BEGIN
         tc::fence_after();
         const uint64_t bT = bU + uint64_t(nb) * b_tile16;
@@ -236,7 +281,7 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t
             tc::mma_i8_elect(tbase + st * kTcTileN, aT + uint64_t(k * 2 * kTcHeads), bT + uint64_t(k * 2 * kTcTileN),
                              idesc, k > 0);
 #endif
-        tc::commit_elect(&sh.tfull[st]);
+        tc::commit_elect_a(bar_at(bars.tfull, st));
         TCP_END(4)
         st ^= 1u;
         tpar ^= st == 0 ? 1u : 0u;
@@ -303,6 +348,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = s_tbase;
+    const TcBars bars(sh);
     const size_t a_slot = size_t(kTcHeads) * kmax;           // bytes per head tile
     const size_t b_buf = size_t(tp.nbt) * kTcTileN * kmax;   // bytes per tail buffer
 
@@ -318,27 +364,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             const uint32_t b_tile16 = uint32_t((size_t(kTcTileN) * kmax) >> 4);
             int ts = 0, cur_bb = -1;
             uint32_t st = 0, tpar = 0;  // next TMEM stage and the parity its tempty wait expects
+#ifdef SDB_TC_GAPS
+            TcGaps gaps;
+#endif
             int uses[2] = {0, 0}, c = 0;
             TCP_DECL
             const unsigned long long tcp_start = clock64();
             for (int u = 0;; u++) {
                 TCP_BEGIN
-                tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
+                tc::mbar_wait_a(bar_at(bars.uqfull, u % kTcUnitQ), (u / kTcUnitQ) & 1);
                 TCP_END(0)
                 const TcUnitDesc d = s_uq[u % kTcUnitQ];
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+                if (lane == 0) tc::mbar_arrive_a(bar_at(bars.uqempty, u % kTcUnitQ));
                 if (d.end) {
+#ifdef SDB_TC_GAPS
+                    if (blockIdx.x == 0 && lane == 0)
+                        printf("[tcgaps] afull wait avg %.1f per tile | in-tile %llu stages avg %.1f (wait %.1f) | tile start %llu avg %.1f (wait %.1f) | unit start %llu avg %.1f (wait %.1f)\n",
+                               double(gaps.afw) / max(1ull, gaps.n[1] + gaps.n[2]),
+                               gaps.n[0], double(gaps.sum[0]) / max(1ull, gaps.n[0]), double(gaps.wait[0]) / max(1ull, gaps.n[0]),
+                               gaps.n[1], double(gaps.sum[1]) / max(1ull, gaps.n[1]), double(gaps.wait[1]) / max(1ull, gaps.n[1]),
+                               gaps.n[2], double(gaps.sum[2]) / max(1ull, gaps.n[2]), double(gaps.wait[2]) / max(1ull, gaps.n[2]));
+#endif
 #ifdef SDB_TC_PROF
                     if (blockIdx.x == 0 && lane == 0) printf("[tcprof] mma: total %llu wait_uq %llu wait_bfull %llu wait_afull %llu wait_tempty %llu issue %llu stages %d\n", clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3], tcp_acc[4], ts);
 #endif
                     break;
                 }
                 if (d.restage) {
-                    if (cur_bb >= 0) tc::commit_elect(&sh.bempty[cur_bb]);  // old buffer free once its MMAs finish
+                    if (cur_bb >= 0) tc::commit_elect_a(bar_at(bars.bempty, cur_bb));  // old buffer free once its MMAs finish
                     cur_bb = d.bb;
                     TCP_BEGIN
-                    tc::mbar_wait(&sh.bfull[cur_bb], uses[cur_bb] & 1);
+                    tc::mbar_wait_a(bar_at(bars.bfull, cur_bb), uses[cur_bb] & 1);
                     TCP_END(1)
                     uses[cur_bb]++;
                 }
@@ -347,20 +404,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 for (int a = 0; a < d.na; a++, c++) {
                     const int s = tc_slot(c);
 #ifndef SDB_TC_MMA_NOAFULL
-                    TCP_BEGIN
-                    tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
-                    TCP_END(2)
+#ifdef SDB_TC_GAPS
+                    const unsigned long long aw0 = clock64();
 #endif
+                    TCP_BEGIN
+                    tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
+                    TCP_END(2)
+#ifdef SDB_TC_GAPS
+                    gaps.afw += clock64() - aw0;
+#endif
+#endif
+#ifdef SDB_TC_FENCE_AFULL  // A/B: the producers' fence.proxy.async + the mbarrier already order the smem writes
                     tc::fence_after();
+#endif
                     const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
                     switch (KT) {
-                        case 1: tc_mma_stages<1>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
-                        case 2: tc_mma_stages<2>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
-                        case 3: tc_mma_stages<3>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
-                        default: tc_mma_stages<4>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, sh TCP_ARGS); break;
+                        case 1: tc_mma_stages<1>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        case 2: tc_mma_stages<2>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        case 3: tc_mma_stages<3>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        default: tc_mma_stages<4>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
                     }
                     ts += d.nbt;
-                    tc::commit_elect(&sh.aempty[s]);
+                    tc::commit_elect_a(bar_at(bars.aempty, s));
                 }
             }
         }
@@ -369,6 +434,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const int q = warp & 3;             // TMEM lane quarter this warp may read
         const int half = (warp - 1) >> 2;   // which 128 columns of a stage
         const int row = 32 * q + lane;      // head row of the tile = TMEM lane
+        const uint32_t ta0 = tbase + (uint32_t(32 * q) << 16) + uint32_t(half * 128);  // + st * 256
         const unsigned sshift = p.scale == 2 ? 1u : 0u;
         unsigned thrH = start_threshold(p, tl.thr0);
         unsigned s_thr_seen = thrH;  // this warp's last bound published to s_thr
@@ -379,11 +445,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const unsigned long long tcp_start = clock64();
         for (int u = 0;; u++) {
             TCP_BEGIN
-            tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
+            tc::mbar_wait_a(bar_at(bars.uqfull, u % kTcUnitQ), (u / kTcUnitQ) & 1);
             TCP_END(0)
             const TcUnitDesc d = s_uq[u % kTcUnitQ];
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+            if (lane == 0) tc::mbar_arrive_a(bar_at(bars.uqempty, u % kTcUnitQ));
             if (d.end) {
 #ifdef SDB_TC_PROF
                 if (blockIdx.x == 0 && lane == 0 && (warp == 1 || warp == 5)) printf("[tcprof] epi warp %d: total %llu wait_uq %llu wait_afull %llu wait_tfull %llu work %llu\n", warp, clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3]);
@@ -404,11 +470,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 const int ch = 0, tenc = 0;
 #else
                 TCP_BEGIN
-                tc::mbar_wait(&sh.afull[s], tc_slot_par(c));
+                tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
                 TCP_END(1)
                 const int ch = s_meta[s].ch[row], tenc = s_meta[s].tenc[row];
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sh.aempty[s]);
+                if (lane == 0) tc::mbar_arrive_a(bar_at(bars.aempty, s));
 #endif
                 const int hoff = row * d.na + a;  // this row's head: rank hbase0 + hoff
                 // other CTAs' finds: the value loaded one head tile ago (its L2 latency hidden
@@ -419,26 +485,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 for (int nb = 0; nb < d.nbt; nb++, ts++) {
                     const int st = ts % kTcStages;
                     TCP_BEGIN
-                    tc::mbar_wait(&sh.tfull[st], (ts / kTcStages) & 1);
+                    tc::mbar_wait_a(bar_at(bars.tfull, st), (ts / kTcStages) & 1);
                     TCP_END(2)
                     TCP_BEGIN
                     tc::fence_after();
-                    const uint32_t ta = tbase + (uint32_t(32 * q) << 16) + uint32_t(st * kTcTileN + half * 128);
-                    uint32_t v[4][16];
-                    tc::ld16_pack(ta, v[0]);
-                    tc::ld16_pack(ta + 32, v[1]);
-                    tc::ld16_pack(ta + 64, v[2]);
-                    tc::ld16_pack(ta + 96, v[3]);
+                    uint32_t v[64];
+                    tc::ld64_pack(ta0 + uint32_t(st * kTcTileN), v);
                     tc::ld_wait();
                     // a pair passes the folded threshold iff its 16-bit accumulator is negative:
-                    // OR the packed words, test the two sign bits
-                    // as a tree of 3-input ORs (depth 4): ptxas turns a plain OR reduction into
-                    // one 32-deep dependent LOP3 chain, which sets the epilogue's latency
+                    // OR the packed words as a tree of 3-input ORs (depth 4; ptxas turns a plain OR
+                    // reduction into one 32-deep dependent LOP3 chain), test the two sign bits
                     uint32_t r[22];
 #pragma unroll
-                    for (int i = 0; i < 21; i++) r[i] = tc::or3(v[(3 * i) >> 4][(3 * i) & 15], v[(3 * i + 1) >> 4][(3 * i + 1) & 15],
-                                                                v[(3 * i + 2) >> 4][(3 * i + 2) & 15]);
-                    r[21] = v[3][15];
+                    for (int i = 0; i < 21; i++) r[i] = tc::or3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+                    r[21] = v[63];
                     uint32_t r2[8];
 #pragma unroll
                     for (int i = 0; i < 7; i++) r2[i] = tc::or3(r[3 * i], r[3 * i + 1], r[3 * i + 2]);
@@ -447,30 +507,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #if defined(SDB_TC_NOMMA) || defined(SDB_TC_NOPROD)
                     o = 0;  // TMEM / the operands hold no real data
 #endif
-                    if (o & 0x80008000u) {
-                        // rare: the exact path for every pair below the folded threshold that
-                        // also passes the current one (val = acc + tenc + 1 <= T)
-                        uint32_t all[64];
+                    if (__any_sync(0xffffffffu, o & 0x80008000u)) {
+                        // rare (warp-uniform: tcgen05.ld is .sync.aligned): re-read the stage
+                        // 32 columns at a time (the values stay in registers, no local copy) and
+                        // take the exact path for every pair below the folded threshold that also
+                        // passes the current one (val = acc + tenc + 1 <= T)
+                        for (int ck = 0; ck < 4; ck++) {
+                            uint32_t w[16];
+                            tc::ld16_pack(ta0 + uint32_t(st * kTcTileN + 32 * ck), w);
+                            tc::ld_wait();
 #pragma unroll
-                        for (int i = 0; i < 16; i++) {
-                            all[i] = v[0][i];
-                            all[16 + i] = v[1][i];
-                            all[32 + i] = v[2][i];
-                            all[48 + i] = v[3][i];
-                        }
-                        for (int x = 0; x < 128; x++) {
-                            const int acc = int(short(all[x >> 1] >> (16 * (x & 1))));
-                            if (acc >= 0 || acc + tenc + 1 > T) continue;
-                            const int y = nb * kTcTileN + half * 128 + x;  // B row of the unit
-                            const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
-                                                d.ntails - 1);
-                            thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoff, tix, thrH);
-                            T = gm.S * int(thrH >> sshift) - gm.C0 - ch;
+                            for (int i = 0; i < 32; i++) {
+                                const int acc = int(short(w[i >> 1] >> (16 * (i & 1))));
+                                if (acc >= 0 || acc + tenc + 1 > T) continue;
+                                const int y = nb * kTcTileN + half * 128 + 32 * ck + i;  // B row of the unit
+                                const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
+                                                    d.ntails - 1);
+                                thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoff, tix, thrH);
+                                T = gm.S * int(thrH >> sshift) - gm.C0 - ch;
+                            }
                         }
                     }
                     tc::fence_before();
                     __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&sh.tempty[st]);
+                    if (lane == 0) tc::mbar_arrive_a(bar_at(bars.tempty, st));
                     TCP_END(3)
                 }
                 // hand a tighter bound to the producers' next head tiles (s_thr_seen is
@@ -532,9 +592,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     st0 = d.t0;
                     visited += (unsigned long long)d.nheads * (unsigned long long)d.ntails;
                 }
-                tc::mbar_wait(&sh.uqempty[u % kTcUnitQ], ((u / kTcUnitQ) & 1) ^ 1);
+                tc::mbar_wait_a(bar_at(bars.uqempty, u % kTcUnitQ), ((u / kTcUnitQ) & 1) ^ 1);
                 s_uq[u % kTcUnitQ] = d;
-                tc::mbar_arrive(&sh.uqfull[u % kTcUnitQ]);
+                tc::mbar_arrive_a(bar_at(bars.uqfull, u % kTcUnitQ));
                 if (d.end) break;
             }
             s_visited = visited;
@@ -549,17 +609,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         int c0 = 0;                                // kernel-wide index of the unit's first head tile
         int fills[2] = {0, 0};
         for (int u = 0;; u++) {
-            tc::mbar_wait(&sh.uqfull[u % kTcUnitQ], (u / kTcUnitQ) & 1);
+            tc::mbar_wait_a(bar_at(bars.uqfull, u % kTcUnitQ), (u / kTcUnitQ) & 1);
             const TcUnitDesc d = s_uq[u % kTcUnitQ];
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sh.uqempty[u % kTcUnitQ]);
+            if (lane == 0) tc::mbar_arrive_a(bar_at(bars.uqempty, u % kTcUnitQ));
             if (d.end) break;
             const TcGammaDev gm = s_gam[d.j];
             const uint32_t *sg = s_sign + size_t(d.j) * N * KW;
             const short *mk = s_mask + d.j * N;
             if (d.restage) {
                 const int bb = d.bb;
-                if (lane == 0) tc::mbar_wait(&sh.bempty[bb], (fills[bb] & 1) ^ 1);
+                if (lane == 0) tc::mbar_wait_a(bar_at(bars.bempty, bb), (fills[bb] & 1) ^ 1);
                 fills[bb]++;
                 __syncwarp();
                 unsigned char *buf = sB + size_t(bb) * b_buf;
@@ -574,20 +634,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #endif
                 tc::fence_async_smem();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sh.bfull[bb]);
+                if (lane == 0) tc::mbar_arrive_a(bar_at(bars.bfull, bb));
             }
 #ifdef SDB_TC_NOPROD
             for (int a = (g - c0) & 1; a < d.na; a += 2) {
                 const int s = tc_slot(c0 + a);
-                if (lane == 0) tc::mbar_wait(&sh.aempty[s], tc_slot_par(c0 + a) ^ 1);
+                if (lane == 0) tc::mbar_wait_a(bar_at(bars.aempty, s), tc_slot_par(c0 + a) ^ 1);
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sh.afull[s]);
+                if (lane == 0) tc::mbar_arrive_a(bar_at(bars.afull, s));
             }
 #else
             switch (tl.h) {
 #define SDB_TC_HEADS(m) \
     case m:                                                                                                \
-        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, sh, &s_thr, sshift); \
+        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, bars, &s_thr, sshift); \
         break;
                 SDB_TC_HEADS(1) SDB_TC_HEADS(2) SDB_TC_HEADS(3) SDB_TC_HEADS(4)
                 SDB_TC_HEADS(5) SDB_TC_HEADS(6) SDB_TC_HEADS(7) SDB_TC_HEADS(8)
