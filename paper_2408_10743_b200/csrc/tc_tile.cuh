@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #ifdef SDB_TC_EPI_NOMETA
             tc::mbar_init(&sh.aempty[s], 1);
 #else
-            tc::mbar_init(&sh.aempty[s], 1 + kTcEpiWarps);   // MMA commit + epilogue (read the slot's meta)
+            tc::mbar_init(&sh.aempty[s], 1 + 32 * kTcEpiWarps);   // MMA commit + every epilogue thread (read the meta)
 #endif
         }
         for (int s = 0; s < 2; s++) {
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         }
         for (int s = 0; s < kTcStages; s++) {
             tc::mbar_init(&sh.tfull[s], 1);
-            tc::mbar_init(&sh.tempty[s], kTcEpiWarps);
+            tc::mbar_init(&sh.tempty[s], 32 * kTcEpiWarps);  // every epilogue thread (no lane test, no warp sync)
         }
         tc::mbar_fence_init();
         s_visited = 0;
@@ -439,7 +439,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         unsigned thrH = start_threshold(p, tl.thr0);
         unsigned s_thr_seen = thrH;  // this warp's last bound published to s_thr
         unsigned wmin_next = thrH;   // the level minimum as loaded at the previous head tile
-        int ts = 0;
+        // the current TMEM stage's full/empty barriers and columns, flipped per stage with XOR
+        // masks (keeps the per-stage loop free of index arithmetic)
+        uint32_t st_e = 0, tpar_e = 0;
+        uint32_t tf_st = bar_at(bars.tfull, 0), te_st = bar_at(bars.tempty, 0), ta_st = ta0;
+        const uint32_t tf_x = tf_st ^ bar_at(bars.tfull, 1), te_x = te_st ^ bar_at(bars.tempty, 1),
+                       ta_x = ta0 ^ (ta0 + uint32_t(kTcTileN));
         int c = 0;  // head tiles consumed
         TCP_DECL
         const unsigned long long tcp_start = clock64();
@@ -473,8 +478,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
                 TCP_END(1)
                 const int ch = s_meta[s].ch[row], tenc = s_meta[s].tenc[row];
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive_a(bar_at(bars.aempty, s));
+                tc::mbar_arrive_a(bar_at(bars.aempty, s));
 #endif
                 const int hoff = row * d.na + a;  // this row's head: rank hbase0 + hoff
                 // other CTAs' finds: the value loaded one head tile ago (its L2 latency hidden
@@ -482,15 +486,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 thrH = min(thrH, wmin_next);
                 wmin_next = ld_relaxed_u32(&p.state->wmin);
                 int T = hoff < d.nheads ? gm.S * int(thrH >> sshift) - gm.C0 - ch : -32768;
-                for (int nb = 0; nb < d.nbt; nb++, ts++) {
-                    const int st = ts % kTcStages;
+                for (int nb = 0; nb < d.nbt; nb++) {
                     TCP_BEGIN
-                    tc::mbar_wait_a(bar_at(bars.tfull, st), (ts / kTcStages) & 1);
+                    tc::mbar_wait_a(tf_st, tpar_e);
                     TCP_END(2)
                     TCP_BEGIN
                     tc::fence_after();
                     uint32_t v[64];
-                    tc::ld64_pack(ta0 + uint32_t(st * kTcTileN), v);
+                    tc::ld64_pack(ta_st, v);
                     tc::ld_wait();
                     // a pair passes the folded threshold iff its 16-bit accumulator is negative:
                     // OR the packed words as a tree of 3-input ORs (depth 4; ptxas turns a plain OR
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                         // passes the current one (val = acc + tenc + 1 <= T)
                         for (int ck = 0; ck < 4; ck++) {
                             uint32_t w[16];
-                            tc::ld16_pack(ta0 + uint32_t(st * kTcTileN + 32 * ck), w);
+                            tc::ld16_pack(ta_st + uint32_t(32 * ck), w);
                             tc::ld_wait();
 #pragma unroll
                             for (int i = 0; i < 32; i++) {
@@ -529,8 +532,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                         }
                     }
                     tc::fence_before();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive_a(bar_at(bars.tempty, st));
+                    tc::mbar_arrive_a(te_st);
+                    // next stage: flip the TMEM stage (and the phase parity after stage 1)
+                    tf_st ^= tf_x;
+                    te_st ^= te_x;
+                    ta_st ^= ta_x;
+                    tpar_e ^= st_e;
+                    st_e ^= 1u;
                     TCP_END(3)
                 }
                 // hand a tighter bound to the producers' next head tiles (s_thr_seen is
