@@ -499,6 +499,11 @@ Plan::~Plan() {
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 void Plan::upload() {
+    // size checks first: a rejected problem must not leave a device block or a pinned image
+    // (with an H2D copy in flight) behind, since ~Plan does not run when the constructor throws
+    if (problem_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024 ||
+        (packaged_ && pkg_smem_bytes(G_, N_, W_, SW_, P_, BK_) > 200 * 1024))
+        throw InvalidArgument("problem too large for shared-memory staging");
     device_ = opts_.device;
     check_cuda(cudaSetDevice(device_), "cudaSetDevice");
     check_cuda(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_), "cudaDeviceGetAttribute");
@@ -570,8 +575,6 @@ void Plan::upload() {
         pk_.P = P_;
         for (int j = 0; j < G_; j++) pk_.np[j] = np_[size_t(j)];
         upload_bytes += h_pk_rows_.size() * 2 + h_pk_size_.size() + h_wsuf_.size() * 8;
-        if (pkg_smem_bytes(G_, N_, W_, SW_, P_, BK_) > 200 * 1024)
-            throw InvalidArgument("problem too large for shared-memory staging");
     }
     upload_bytes += h_prows_.size() * 4;
     if (tc_ok_) {
@@ -592,8 +595,6 @@ void Plan::upload() {
     pd_.max_weight = max_weight_;
     levels_.assign(size_t(N_ + 1), LevelHost{});
     events_.assign(size_t(2 * (N_ + 1)), nullptr);
-    if (problem_smem_bytes(G_, N_, W_, SW_, BK_) > 200 * 1024)
-        throw InvalidArgument("problem too large for shared-memory staging");
 }
 
 cudaEvent_t Plan::level_event(int i) {
@@ -627,7 +628,7 @@ static void forced_tile(int g, int &t, int &tchunk) {
 constexpr double kTileUnitCost = 40000;
 constexpr double kTileTailFraction = 0.4;
 
-TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
+TileChoice choose_tile(int G, int N, int g, int W, int K, unsigned long long per_gamma, int forced_kernel, int num_sms,
                        int world) {
     TileChoice best{0, kTailChunk};
     if (forced_kernel == 1 || g < 2) return best;
@@ -638,9 +639,10 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
     // padded candidates (every lane of a warp with heads runs H heads) plus kTileUnitCost for
     // the dispenser, tail staging and head generation; the walk kernel costs ~28 per candidate
     // (measured 1.4e11 vs 3.9e12 cand/s) with perfectly fine granularity.
-    const int K = probe_words(W, false);
+    // K: the launched kernel's probe words per row (W, or W + 1 with the extra probe word): it
+    // sets the heads per lane, the head block and the CTAs per SM
     const double Hl = heads_per_lane(W, K), HBk = head_block(W, K);
-    const double slots = double(num_sms) * tile_blocks_per_sm(W, probe_words(W, false)) * std::max(1, world);  // all ranks' CTAs
+    const double slots = double(num_sms) * tile_blocks_per_sm(W, K) * std::max(1, world);  // all ranks' CTAs
     std::vector<double> C(size_t(N + 1) * size_t(N + 1), 0.0);  // Pascal's triangle in doubles
     for (int a = 0; a <= N; a++)
         for (int k = 0; k <= a; k++)
@@ -678,7 +680,7 @@ TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma,
 }
 
 int choose_tile_t(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel) {
-    return choose_tile(G, N, g, W, per_gamma, forced_kernel, 148, 1).t;
+    return choose_tile(G, N, g, W, probe_words(W, false), per_gamma, forced_kernel, 148, 1).t;
 }
 
 // Cost model of the tensor-core tile kernel, in SM cycles per CTA (one CTA per SM). A unit
@@ -811,7 +813,7 @@ bool Plan::prepare_ptile(int g, LevelHost &lv, int world, int rank) {
     const unsigned long long total = level_candidates(g);
     if (opts_.kernel != 2 && total < (1ull << 16)) return false;
     const double Hl = heads_per_lane(W_, pd_.K), HBk = head_block(W_, pd_.K);
-    const double slots = double(num_sms_) * tile_blocks_per_sm(W_, probe_words(W_, false)) * std::max(1, world);
+    const double slots = double(num_sms_) * tile_blocks_per_sm(W_, pd_.K) * std::max(1, world);
     double best_time = opts_.kernel == 2 ? 1e300 : double(total) * 28.0 / slots;
     int best_t = 0, best_chunk = kTailChunk;
     auto Hb_of = [&](int j, int b, int h) { return double(F_at(j, h_off_[size_t(j) * (P_ + 1) + b], h)); };
@@ -911,6 +913,11 @@ void Plan::prepare_level(int g) {
     const int world = lv.sharded ? std::max(1, opts_.world) : 1, rank = lv.sharded ? opts_.rank : 0;
     if (packaged_) {
         if (g >= BK_) throw InvalidArgument("generation beyond the kernels' combination-size limit");
+        // both packaged kernels key a candidate as Gamma << 58 | rank: check every Gamma's
+        // level size before either is prepared
+        for (int j = 0; j < G_; j++)
+            if (h_wsuf_[size_t(j) * (P_ + 1) * BK_ + size_t(g)] >= (1ull << kKeyRankBits))
+                throw InvalidArgument("level too large for 58-bit combination ranks");
         if (prepare_ptile(g, lv, world, rank)) {
             lv.ready = true;
             return;
@@ -950,7 +957,7 @@ void Plan::prepare_level(int g) {
         lv.ready = true;
         return;
     }
-    TileChoice tc = choose_tile(G_, N_, g, W_, per, opts_.kernel, num_sms_, world);
+    TileChoice tc = choose_tile(G_, N_, g, W_, K_, per, opts_.kernel, num_sms_, world);
     forced_tile(g, tc.t, tc.tchunk);
     lv.t = tc.t;
     if (lv.t == 0) {
@@ -1091,13 +1098,41 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     check_cuda(cudaGetLastError(), "run init launch");
     RunCtl ctl{};
     std::vector<unsigned char> h_state;
+    bool stopped_early = false;  // a deferred check found the run done while level g failed to set up
     for (int g = 1; g <= g_limit; g++) {
-        prepare_level(g);
+        // Level g is set up before the previous big level's check resolves (deferred check).
+        // If the setup fails (size limits, launch errors), resolve that check first: a run
+        // that already terminated must report its result, not this level's error.
+        try {
+            prepare_level(g);
+        } catch (...) {
+            if (pending_g) {
+                check_cuda(cudaEventSynchronize(check_ev), "level check");
+                pending_g = 0;
+                if (h_ctl_->done) {
+                    stopped_early = true;
+                    break;
+                }
+            }
+            throw;
+        }
         const LevelHost &lv = levels_[size_t(g)];
         // per-level events only when the caller wants per-level times; else one pair
         // around all levels (fewer API calls on small codes)
         if (level_seconds || g == 1) check_cuda(cudaEventRecord(level_event(2 * g), stream_), "event");
-        launches += launch_level(g);
+        try {
+            launches += launch_level(g);
+        } catch (...) {
+            if (pending_g) {
+                check_cuda(cudaEventSynchronize(check_ev), "level check");
+                pending_g = 0;
+                if (h_ctl_->done) {
+                    stopped_early = true;
+                    break;
+                }
+            }
+            throw;
+        }
         int from_keys = 0;
         if (lv.sharded && opts_.comm) {
             // stream-ordered NCCL min-allreduce of the per-weight best keys; level_close reads
@@ -1160,6 +1195,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
         if (!packaged_ && g == kMaxLevel && g < N_ && (opts_.max_generation <= 0 || opts_.max_generation > g))
             throw InvalidArgument("generation beyond the kernels' combination-size limit");
     }
+    (void)stopped_early;  // the trace below ends at the last level launched either way
     if (!level_seconds) check_cuda(cudaEventRecord(level_event(1), stream_), "event");
     std::vector<int> tu(size_t(last_g + 1));
     check_cuda(cudaMemcpyAsync(&ctl, pd_.ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream_), "D2H ctl");

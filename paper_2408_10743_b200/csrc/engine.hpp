@@ -146,7 +146,7 @@ struct TileChoice {
     int t;       // 0: walk kernel
     int tchunk;  // tails per unit
 };
-TileChoice choose_tile(int G, int N, int g, int W, unsigned long long per_gamma, int forced_kernel, int num_sms,
+TileChoice choose_tile(int G, int N, int g, int W, int K, unsigned long long per_gamma, int forced_kernel, int num_sms,
                        int world);
 // levels with fewer candidates run whole on every rank (RunOptions.shard_min = 0)
 constexpr unsigned long long kDefaultShardMin = 1ull << 26;
