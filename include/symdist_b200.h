@@ -142,7 +142,12 @@ typedef struct {
     unsigned long long d2h_bytes;        /* device->host bytes this call moved */
     int last_level_kernel;               /* kernel of the last level run: 1 walk, 2 POPC tile,
                                             3 tensor-core tile, 4 package walk, 5 package tile */
-    int reserved[3];
+    int reserved;
+    unsigned long long candidates_skipped; /* left out by the mid-level early exit: once a level's
+                                              minimum reaches L(g-1) it is the distance, and
+                                              work whose keys all exceed the best key cannot
+                                              change trace or best; visited + skipped =
+                                              enumerated on a single rank */
 } sdb_report;
 
 void sdb_default_options(sdb_run_options *opts);

@@ -123,7 +123,7 @@ class _Report(C.Structure):
         ("candidates_visited", C.c_ulonglong), ("prep_seconds", C.c_double), ("enum_seconds", C.c_double),
         ("n_gammas", C.c_int), ("kernel_launches", C.c_int), ("best_generation", C.c_int), ("best_gamma", C.c_int),
         ("best_rank", C.c_ulonglong), ("h2d_bytes", C.c_ulonglong), ("d2h_bytes", C.c_ulonglong),
-        ("last_level_kernel", C.c_int), ("reserved", C.c_int * 3),
+        ("last_level_kernel", C.c_int), ("reserved", C.c_int), ("candidates_skipped", C.c_ulonglong),
     ]
 
 
@@ -324,6 +324,7 @@ class DistanceReport:
     d2h_bytes: int = 0
     level_seconds: list = field(default_factory=list)
     last_level_kernel: int = 0  # 1 walk, 2 POPC tile, 3 tensor-core tile, 4 package walk, 5 package tile
+    candidates_skipped: int = 0  # left out by the mid-level early exit (visited + skipped = enumerated)
 
     def trace_tuples(self):
         return [e.astuple() for e in self.bounds_trace]
@@ -340,7 +341,7 @@ def _report(r: _Report, tr, cap: int) -> DistanceReport:
         prep_seconds=r.prep_seconds, enum_seconds=r.enum_seconds, n_gammas=r.n_gammas,
         kernel_launches=r.kernel_launches, best_generation=r.best_generation, best_gamma=r.best_gamma,
         best_rank=int(r.best_rank), h2d_bytes=int(r.h2d_bytes), d2h_bytes=int(r.d2h_bytes),
-        last_level_kernel=r.last_level_kernel)
+        last_level_kernel=r.last_level_kernel, candidates_skipped=int(r.candidates_skipped))
 
 
 _TRACE_CAP = 512

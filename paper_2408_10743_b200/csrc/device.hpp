@@ -36,6 +36,7 @@ struct LevelState {
     unsigned int wmin;           // min weight found this level (engine units), ~0u: none
     unsigned int pad;
     unsigned long long visited;  // candidates the kernels enumerated
+    unsigned long long skipped;  // candidates left out by the mid-level early exit (early_skip)
     // followed in memory by key_by_w[max_weight + 1] (u64)
 };
 
@@ -50,6 +51,7 @@ struct RunCtl {
     int pad;
     unsigned long long best_key;    // gamma << 58 | lexicographic rank
     unsigned long long visited;     // candidates the kernels enumerated, all levels
+    unsigned long long skipped;     // candidates the mid-level early exit left out, all levels
 };
 
 struct ProblemDev {
@@ -76,6 +78,7 @@ struct LevelLaunch {
     // sharding: this rank takes segments rank, rank + world, ... of [0, seg_total)
     unsigned long long seg_total;
     int shard_rank, shard_world;
+    unsigned int lprev;           // L(g - 1): the mid-level early exit's bound (0: off)
 };
 
 // Level-loop control kernels (one CTA each): reset U / best / counters for a run, and
@@ -165,6 +168,7 @@ struct TilePlan {
     unsigned long long unit_total;
     int shard_rank, shard_world;
     unsigned long long per_gamma;   // C(N, g): lexicographic-rank base
+    unsigned int lprev;             // L(g - 1): the mid-level early exit's bound (0: off)
 };
 int launch_tile_level(const ProblemDev &p, const TilePlan &tp, void *stream, int num_sms);
 
@@ -281,6 +285,7 @@ struct PkgLevel {
     unsigned long long segs[kMaxPkgG];   // segments of each Gamma
     unsigned long long seg_total;
     int shard_rank, shard_world;
+    unsigned int lprev;           // L(g - 1): the mid-level early exit's bound (0: off)
 };
 size_t pkg_smem_bytes(int G, int N, int W, int SW, int P, int BK);
 

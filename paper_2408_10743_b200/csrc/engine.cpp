@@ -734,6 +734,14 @@ TcChoice choose_tc(int G, int N, int g, const std::vector<TcGammaDev> &gam, int 
     return best;
 }
 
+// L(g - 1) for the kernels' mid-level early exit (kernels.cu early_key); 0 turns it off: for
+// g = 1, and for the single-level seam (run_level), whose caller's bound state it cannot see
+unsigned Plan::early_bound(int g) const {
+    if (g < 2 || single_level_) return 0;
+    const long long L = lower_bound(g - 1);
+    return L <= 0 ? 0u : unsigned(std::min<long long>(L, 0x7fffffffLL));
+}
+
 bool Plan::prepare_tc(int g, LevelHost &lv, int world, int rank) {
     TcChoice c = choose_tc(G_, N_, g, tc_enc_.gam, tc_enc_.kmax, tc_enc_.kw, W_, BK_, num_sms_, world);
     if (const char *force = std::getenv("SDB_TC_FORCE")) {  // experiments: "g:t:nbt,..."
@@ -751,6 +759,7 @@ bool Plan::prepare_tc(int g, LevelHost &lv, int world, int rank) {
     TcPlan &tp = lv.tc;
     TilePlan &tl = tp.tile;
     tl.g = g;
+    tl.lprev = early_bound(g);
     tl.t = c.t;
     tl.h = g - c.t;
     tl.thr0 = ~0u;
@@ -963,6 +972,7 @@ void Plan::prepare_level(int g) {
     if (lv.t == 0) {
         LevelLaunch &LL = lv.walk;
         LL.g = g;
+        LL.lprev = early_bound(g);
         LL.thr0 = ~0u;  // the kernels read U from the device (RunCtl)
         LL.per_gamma = per;
         const unsigned long long threads_total = (unsigned long long)num_sms_ * 8 * 256;
@@ -978,6 +988,7 @@ void Plan::prepare_level(int g) {
     } else {
         TilePlan &tp = lv.tile;
         tp.g = g;
+        tp.lprev = early_bound(g);
         tp.t = lv.t;
         tp.h = g - lv.t;
         tp.thr0 = ~0u;
@@ -1044,6 +1055,7 @@ bool Plan::run_level(int g, long long upper, long long *upper_out, unsigned long
     const unsigned start = unsigned(std::min<long long>(upper, sentinel_));
     launch_run_init(pd_, start, d_counter_init_, d_counters_, N_ + 1, stream_);
     check_cuda(cudaGetLastError(), "run init launch");
+    single_level_ = true;
     prepare_level(g);
     launch_level(g);
     launch_level_close(pd_, g, 0, 0, stream_);  // lower 0: the close never terminates
@@ -1242,6 +1254,7 @@ void Plan::run(sdb_report *rep, sdb_trace_entry *trace, int trace_cap, uint64_t 
     rep->complete = complete ? 1 : 0;
     rep->upper = U;
     rep->candidates_visited = ctl.visited;
+    rep->candidates_skipped = ctl.skipped;
     rep->enum_seconds = enum_s;
     rep->n_gammas = G_;
     rep->kernel_launches = launches;

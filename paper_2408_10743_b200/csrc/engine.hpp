@@ -84,6 +84,7 @@ class Plan {
     void upload();
     int launch_level(int g);  // the level's kernel(s) on the plan's stream; returns the launch count
     long long lower_bound(int g) const;
+    unsigned early_bound(int g) const;
     void prepare_level(int g);
     bool prepare_ptile(int g, LevelHost &lv, int world, int rank);
     bool prepare_tc(int g, LevelHost &lv, int world, int rank);
@@ -98,6 +99,7 @@ class Plan {
     std::vector<uint32_t> h_rows_;
     std::vector<uint32_t> h_prows_;  // [G][N][K_] the tile kernels' probe words
     int K_ = 1;
+    bool single_level_ = false;  // run_level (the enumerate_generation seam): no early exit
     std::vector<uint64_t> h_syn_;
     std::vector<unsigned long long> h_binom_;
     int device_ = 0, num_sms_ = 148;

@@ -84,6 +84,18 @@ __device__ __forceinline__ bool admissible_combo(const unsigned long long *syn, 
 __device__ __forceinline__ bool run_done(const ProblemDev &p) { return *(volatile int *)&p.ctl->done != 0; }
 
 // threshold at kernel start: weights <= U - 1 can still lower U (engine units)
+// Mid-level early exit. Every codeword not enumerated by levels < g weighs at least L(g-1),
+// and U > L(g-1) when level g starts, so a level-g candidate never weighs less than L(g-1);
+// once the level minimum reaches L(g-1) it is the distance and level g's close will stop the
+// run with the same (g, L, U). What may still change is `best`, the first minimal candidate in
+// the reference's order (Gamma, lexicographic rank): work whose keys all exceed the current
+// key of that weight cannot lower it. Returns that key, or ~0 while the exit does not apply.
+__device__ __forceinline__ unsigned long long early_key(const ProblemDev &p, unsigned lprev) {
+    const unsigned w = *(volatile unsigned *)&p.state->wmin;
+    if (lprev == 0 || w > lprev) return ~0ull;
+    return *(volatile unsigned long long *)&p.key_by_w[w];
+}
+
 __device__ __forceinline__ unsigned start_threshold(const ProblemDev &p, unsigned thr0) {
     const unsigned U = *(volatile unsigned *)&p.ctl->U;
     return min(min(thr0, U - 1u), *(volatile unsigned *)&p.state->wmin);
@@ -97,8 +109,10 @@ __global__ void run_init_kernel(ProblemDev p, unsigned sentinel, const unsigned 
         p.ctl->best_g = -1;
         p.ctl->best_key = ~0ull;
         p.ctl->visited = 0;
+        p.ctl->skipped = 0;
         p.state->wmin = ~0u;
         p.state->visited = 0;
+        p.state->skipped = 0;
     }
     for (int i = threadIdx.x; i <= p.max_weight; i += blockDim.x) p.key_by_w[i] = ~0ull;
     for (int i = threadIdx.x; i <= p.N; i += blockDim.x) p.trace_upper[i] = -1;
@@ -129,10 +143,12 @@ __global__ void level_close_kernel(ProblemDev p, int g, long long lower, int fro
             }
             p.trace_upper[g] = int(c->U);
             c->visited += p.state->visited;
+            c->skipped += p.state->skipped;
             if (lower >= (long long)c->U) c->done = 1;
         }
         p.state->wmin = ~0u;
         p.state->visited = 0;
+        p.state->skipped = 0;
     }
     __syncthreads();
     for (int i = threadIdx.x; i <= p.max_weight; i += blockDim.x) p.key_by_w[i] = ~0ull;
@@ -159,7 +175,7 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
 
     const int g = L.g, N = p.N;
     unsigned int thr = start_threshold(p, L.thr0);
-    unsigned long long visited = 0;
+    unsigned long long visited = 0, skipped = 0;
     int c[kMaxLevel];
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long it = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;; it += stride) {
@@ -168,6 +184,10 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
         const int j = int(seg / L.segs_per_gamma);
         const unsigned long long r0 = (seg % L.segs_per_gamma) * L.seg_len;
         const unsigned long long r1 = min(r0 + L.seg_len, L.per_gamma);
+        if ((((unsigned long long)j << kKeyRankBits) | r0) > early_key(p, L.lprev)) {
+            skipped += r1 - r0;  // every key of the segment exceeds the best one (early exit)
+            continue;
+        }
         const uint32_t *grows = s_rows + j * N * rowlen;
         const unsigned long long *gsyn = s_syn + j * N * p.SW;
         unrank_lex(r0, g, N, s_binom, BKs, c);
@@ -198,8 +218,12 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
         thr = min(thr, *(volatile unsigned int *)&p.state->wmin);
     }
     // one atomic per warp for the visit counter
-    for (int o = 16; o > 0; o >>= 1) visited += __shfl_down_sync(0xffffffffu, visited, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        visited += __shfl_down_sync(0xffffffffu, visited, o);
+        skipped += __shfl_down_sync(0xffffffffu, skipped, o);
+    }
     if ((threadIdx.x & 31) == 0 && visited) atomicAdd(&p.state->visited, visited);
+    if ((threadIdx.x & 31) == 0 && skipped) atomicAdd(&p.state->skipped, skipped);
 }
 
 // ---------------------------------------------------------------- packages (1/3-packages)
@@ -851,7 +875,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_word
     uint32_t *s_tp = reinterpret_cast<uint32_t *>(smem + lay.tp);
     uint32_t *s_prows = reinterpret_cast<uint32_t *>(smem + lay.prows);
     __shared__ TileUnit s_un;
-    __shared__ unsigned long long s_visited;
+    __shared__ unsigned long long s_visited, s_skipped;
     // units are claimed in runs of consecutive indices (fewer near the end of the level); the
     // head blocks of one tail chunk are consecutive, so a run mostly reuses the staged tails
     __shared__ unsigned long long s_claim, s_claim_end;
@@ -866,6 +890,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_word
     for (int i = threadIdx.x; i < nbinom; i += blockDim.x) s_binom[i] = p.binom[(i / BKs) * p.BK + i % BKs];
     if (threadIdx.x == 0) {
         s_visited = 0;
+        s_skipped = 0;
         s_claim = s_claim_end = 0;
         s_staged_b = -1;
     }
@@ -913,18 +938,25 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_word
                 s_un.tcount = int(min((unsigned long long)tp.tchunk, Tb - s_un.t0));
                 s_un.hbase0 = hc * HB;
                 s_un.pad = int(min((unsigned long long)HB, Hb - hc * HB));  // heads in this block
-                s_visited += (unsigned long long)s_un.pad * (unsigned long long)s_un.tcount;
-                if (s_un.j != s_staged_j || b != s_staged_b || s_un.t0 != s_staged_t0) {
-                    s_restage = 1;
-                    s_staged_j = s_un.j;
-                    s_staged_b = b;
-                    s_staged_t0 = s_un.t0;
+                if ((unsigned long long)s_un.j > (early_key(p, tp.lprev) >> kKeyRankBits)) {
+                    // early exit: a later Gamma's keys all exceed the best one; -1 skips the unit
+                    s_skipped += (unsigned long long)s_un.pad * (unsigned long long)s_un.tcount;
+                    s_un.tcount = -1;
+                } else {
+                    s_visited += (unsigned long long)s_un.pad * (unsigned long long)s_un.tcount;
+                    if (s_un.j != s_staged_j || b != s_staged_b || s_un.t0 != s_staged_t0) {
+                        s_restage = 1;
+                        s_staged_j = s_un.j;
+                        s_staged_b = b;
+                        s_staged_t0 = s_un.t0;
+                    }
                 }
             }
         }
         __syncthreads();
         const int tcount = s_un.tcount;
         if (tcount == 0) break;
+        if (tcount < 0) continue;  // skipped (the loop top syncs before s_un is rewritten)
         const int t = tp.t, h = tp.h;
         {
             const int b = s_un.b;
@@ -1048,6 +1080,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_blocks_per_sm(W, probe_word
         }
         thrH = min(thrH, *(volatile unsigned int *)&p.state->wmin);
     }
+    if (threadIdx.x == 0 && s_skipped) atomicAdd(&p.state->skipped, s_skipped);
     if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
 }
 

@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 (tl.unit_total + tl.shard_world - 1 - tl.shard_rank) / tl.shard_world;
             constexpr int kHB = kTcHeads * kTcUnitTiles;  // heads per unit
             int cur_bb = -1, sj = -1, sb = -1;
-            unsigned long long st0 = 0, claim = 0, claim_end = 0, seen = 0, visited = 0;
+            unsigned long long st0 = 0, claim = 0, claim_end = 0, seen = 0, visited = 0, skipped = 0;
             int lo = 0;  // (Gamma, b) index of the previous unit: units of a run mostly share it
             for (int u = 0;; u++) {
                 TcUnitDesc d{};
@@ -592,6 +592,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     d.hbase0 = hc * kHB;
                     d.nheads = int(min((unsigned long long)kHB, Hb - d.hbase0));
                     d.na = (d.nheads + kTcHeads - 1) / kTcHeads;
+                    if ((unsigned long long)d.j > (early_key(p, tl.lprev) >> kKeyRankBits)) {
+                        // mid-level early exit: a later Gamma's keys all exceed the best one
+                        skipped += (unsigned long long)d.nheads * (unsigned long long)d.ntails;
+                        u--;  // nothing published for this claim
+                        continue;
+                    }
                     d.restage = d.j != sj || b != sb || d.t0 != st0;
                     if (d.restage) cur_bb = cur_bb < 0 ? 0 : cur_bb ^ 1;
                     d.bb = cur_bb;
@@ -606,6 +612,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 if (d.end) break;
             }
             s_visited = visited;
+            if (skipped) atomicAdd(&p.state->skipped, skipped);
         }
     } else {
         // ------------------------------------------------------------ producers
