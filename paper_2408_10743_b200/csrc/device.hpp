@@ -23,6 +23,23 @@
 #define SDB_HD
 #endif
 
+// Bounds checks of the kernels' shared-memory and combination indexing, compiled in only for
+// the checked build (tools/build_variant.sh checked "-DSDB_DEBUG_CHECKS", run under the GPU
+// test suite with SDB_TEST_VARIANT=checked): compute-sanitizer is not available on the GPU
+// pool, so out-of-range indices trap here instead.
+#if defined(SDB_DEBUG_CHECKS) && defined(__CUDA_ARCH__)
+#define SDB_CHECK(cond)                                                                          \
+    do {                                                                                         \
+        if (!(cond)) {                                                                           \
+            printf("SDB_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   int(blockIdx.x), int(threadIdx.x));                                           \
+            __trap();                                                                            \
+        }                                                                                        \
+    } while (0)
+#else
+#define SDB_CHECK(cond) ((void)0)
+#endif
+
 namespace sdb {
 
 constexpr int kMaxW = 8;         // u32 words per half: n <= 256

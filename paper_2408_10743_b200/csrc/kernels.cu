@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(256) walk_kernel(ProblemDev p, LevelLaunch L) 
         const uint32_t *grows = s_rows + j * N * rowlen;
         const unsigned long long *gsyn = s_syn + j * N * p.SW;
         unrank_lex(r0, g, N, s_binom, BKs, c);
+        for (int i = 0; i < g; i++) SDB_CHECK(c[i] >= 0 && c[i] < N && (i == 0 || c[i] > c[i - 1]));
         uint32_t acc[2 * W];
 #pragma unroll
         for (int i = 0; i < 2 * W; i++) acc[i] = 0;
@@ -797,6 +798,7 @@ __device__ __noinline__ unsigned tile_exact(const ProblemDev p, const TilePlan t
     c[h] = b;
     unrank_colex_est(un->t0 + tix, t - 1, N - 1 - b, s_binom, BKs, c + h + 1);
     for (int k = h + 1; k < g; k++) c[k] += b + 1;
+    for (int k = 0; k < g; k++) SDB_CHECK(c[k] >= 0 && c[k] < N && (k == 0 || c[k] > c[k - 1]));
     uint32_t acc[2 * W];
 #pragma unroll
     for (int w = 0; w < 2 * W; w++) acc[w] = 0;

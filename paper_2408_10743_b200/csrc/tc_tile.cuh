@@ -151,6 +151,7 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
         const int y = r * (kTcProdWarps * 32) + pq;  // B row
         unsigned char *tile = buf + size_t(y / kTcTileN) * kTcTileN * kmax;
         const int trow = y % kTcTileN;
+        SDB_CHECK(y < R * kTcTileN && b + 1 + (T1 > 0 ? e[T1 - 1] : 0) < N);
 #pragma unroll
         for (int w = 0; w < KW; w++)
             if (w < gm.K / 32) tc_store_block<false>(tile, kTcTileN, trow, w, sw[w], gm.W1);
@@ -189,6 +190,7 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
         int cnt;
         tc_gather<H, KW, false>(sg, mk, 0, 0, e, sw, cnt);
         const int c = c0 + a, s = tc_slot(c);
+        SDB_CHECK(s >= 0 && s < kTcSlots && (H == 0 || e[H - 1] < d.b) && pt < kTcHeads);
         if (lane == 0) tc::mbar_wait_a(bar_at(bars.aempty, s), tc_slot_par(c) ^ 1);
         __syncwarp();
         unsigned char *tile = sA + size_t(s) * a_slot;
@@ -526,6 +528,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                                 const int y = nb * kTcTileN + half * 128 + 32 * ck + i;  // B row of the unit
                                 const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
                                                     d.ntails - 1);
+                                SDB_CHECK(tix >= 0 && tix < d.ntails && hoff < d.nheads);
                                 thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoff, tix, thrH);
                                 T = gm.S * int(thrH >> sshift) - gm.C0 - ch;
                             }
@@ -578,6 +581,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                         }
                         lo = l;
                     }
+                    SDB_CHECK(lo >= 0 && lo < G * tl.nb && s_cum[lo] <= unit && unit < s_cum[lo + 1]);
                     const int b = tl.h + lo % tl.nb;
                     const unsigned long long uu = unit - s_cum[lo];
                     const unsigned long long Hb = binom_at(s_binom, BKs, b, tl.h);

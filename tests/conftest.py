@@ -39,6 +39,11 @@ def gpu():
     only runs on the GPU box, where a silent skip would hide a broken build."""
     import paper_2408_10743_b200 as P
 
+    # SDB_TEST_VARIANT=checked runs the suite on the bounds-checked build (SDB_DEBUG_CHECKS,
+    # tools/build_variant.sh), standing in for compute-sanitizer, which the GPU pool lacks
+    variant = os.environ.get("SDB_TEST_VARIANT")
+    if variant:
+        P.use_variant_library(os.path.join(ROOT, "paper_2408_10743_b200", "_variants", variant, "libsymdist_b200.so"))
     if not P.device_available():
         pytest.fail("no usable CUDA device: " + P.library().sdb_last_error().decode())
     return P
