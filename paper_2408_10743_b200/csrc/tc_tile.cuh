@@ -151,7 +151,7 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
         const int y = r * (kTcProdWarps * 32) + pq;  // B row
         unsigned char *tile = buf + size_t(y / kTcTileN) * kTcTileN * kmax;
         const int trow = y % kTcTileN;
-        SDB_CHECK(y < R * kTcTileN && b + 1 + (T1 > 0 ? e[T1 - 1] : 0) < N);
+        SDB_CHECK(y < R * kTcTileN && (T1 > 0 ? b + 1 + e[T1 - 1] : b) < N);
 #pragma unroll
         for (int w = 0; w < KW; w++)
             if (w < gm.K / 32) tc_store_block<false>(tile, kTcTileN, trow, w, sw[w], gm.W1);
