@@ -218,7 +218,8 @@ constexpr int kTcUnitQ = 8;        // unit descriptors in flight
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcThreads = 32 * (1 + kTcEpiWarps + 1 + kTcProdWarps);
 constexpr int kTcMaxK = 128;       // coordinates per operand row
-constexpr int kTcMaxNbt = 6;       // B tiles per unit
+constexpr int kTcMaxNbt = 12;      // B tiles per unit (tail tiles a head tile meets)
+constexpr int kTcMaxBSlots = kTcMaxNbt + 1;  // B tile ring: one spare slot lets the next chunk start early
 struct TcGammaDev {
     int K;       // coordinates of this Gamma (multiple of 32; MMA K steps = K / 32)
     int W1;      // 4-coordinate words whose tail coefficient is alpha (S = 4: 2), the rest 1
@@ -235,7 +236,7 @@ struct TcGammaDev {
 // stores conflict-free).
 struct TcUnitDesc {
     unsigned long long hbase0, t0;
-    int j, b, nheads, ntails, nbt, na, bb, restage, end, pad;
+    int j, b, nheads, ntails, nbt, na, chunk_last, restage, end, pad;  // chunk_last: the next unit restages
 };
 struct TcSlotMeta {
     short ch[kTcHeads];    // per head row: alpha * |S_h ∩ mask rows|
@@ -265,7 +266,7 @@ SDB_HD inline TcSmem tc_smem_layout(int G, int N, int W, int kmax, int kw, int n
     TcSmem L{};
     L.a = 0;
     L.b = L.a + size_t(kTcSlots) * kTcHeads * kmax;
-    L.sign = L.b + size_t(2) * nbt * kTcTileN * kmax;
+    L.sign = L.b + size_t(nbt + 1) * kTcTileN * kmax;  // the B ring: nbt + 1 tail tiles
     L.mask = align16(L.sign + size_t(G) * N * kw * 4);
     L.rows = align16(L.mask + size_t(G) * N * 2);
     L.binom = align16(L.rows + size_t(G) * N * 2 * W * 4);

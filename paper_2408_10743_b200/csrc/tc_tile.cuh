@@ -114,7 +114,8 @@ __device__ __forceinline__ int tc_slot(int c) { return c % kTcSlots; }
 __device__ __forceinline__ uint32_t tc_slot_par(int c) { return (c / kTcSlots) & 1; }
 
 struct TcShared {
-    uint64_t uqfull[kTcUnitQ], uqempty[kTcUnitQ], afull[kTcSlots], aempty[kTcSlots], bfull[2], bempty[2],
+    uint64_t uqfull[kTcUnitQ], uqempty[kTcUnitQ], afull[kTcSlots], aempty[kTcSlots], bfull[kTcMaxBSlots],
+        bempty[kTcMaxBSlots],
         tfull[kTcStages], tempty[kTcStages];
 };
 // shared-window addresses of the mbarrier arrays (bar i of an array at base + 8 i), computed
@@ -135,23 +136,29 @@ struct TcBars {
 };
 __device__ __forceinline__ uint32_t bar_at(uint32_t base, int i) { return base + 8u * uint32_t(i); }
 
-// Producer thread pq (0..255): this unit's tails pq * nbt .. + nbt - 1 into B rows r * 256 + pq.
+// Producer thread pq (0..255): this unit's tails pq * nbt .. + nbt - 1, tail pq * nbt + r into
+// row pq of the chunk's tile r. Tile r is ring fill Fc + r: slot (Fc + r) % nsb, written once
+// the MMA released that slot's previous fill (sempty), announced with sfull per tile.
 template <int T1, int KW>
-__device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq, int N, int kmax,
+__device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq, int lane, int N, int kmax,
                                const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
-                               unsigned char *buf) {
+                               unsigned char *sB, unsigned long long Fc, int nsb, const TcBars &bars) {
     const int b = d.b, R = d.nbt, i0 = pq * R;
     int e[kTcMaxPart];
     tc_unrank<T1>(d.t0 + min(i0, d.ntails - 1), N - 1 - b, binom, BKs, e);
+    int slot = int(Fc % unsigned(nsb));
+    uint32_t epar = uint32_t((Fc / unsigned(nsb)) & 1u) ^ 1u;  // parity of the release a fill waits for
+    const size_t tile_bytes = size_t(kTcTileN) * kmax;
     for (int r = 0; r < R; r++) {
         if (r > 0 && i0 + r < d.ntails) tc_succ<T1>(e);
         uint32_t sw[KW];
         int cnt;
         tc_gather<T1, KW, true>(sg, mk, b + 1, b, e, sw, cnt);
-        const int y = r * (kTcProdWarps * 32) + pq;  // B row
-        unsigned char *tile = buf + size_t(y / kTcTileN) * kTcTileN * kmax;
-        const int trow = y % kTcTileN;
-        SDB_CHECK(y < R * kTcTileN && (T1 > 0 ? b + 1 + e[T1 - 1] : b) < N);
+        SDB_CHECK(slot >= 0 && slot < nsb && (T1 > 0 ? b + 1 + e[T1 - 1] : b) < N);
+        if (lane == 0) tc::mbar_wait_a(bar_at(bars.bempty, slot), epar);
+        __syncwarp();
+        unsigned char *tile = sB + size_t(slot) * tile_bytes;
+        const int trow = pq;
 #pragma unroll
         for (int w = 0; w < KW; w++)
             if (w < gm.K / 32) tc_store_block<false>(tile, kTcTileN, trow, w, sw[w], gm.W1);
@@ -164,6 +171,13 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
         tile[tc::kmajor_off(kTcTileN, trow, gm.kc)] = (unsigned char)(-(gm.alpha * cnt));
         tile[tc::kmajor_off(kTcTileN, trow, gm.kt)] = 1;
         tile[tc::kmajor_off(kTcTileN, trow, gm.kt + 1)] = 16;
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_a(bar_at(bars.bfull, slot));
+        if (++slot == nsb) {
+            slot = 0;
+            epar ^= 1u;
+        }
     }
 }
 
@@ -173,15 +187,16 @@ template <int H, int KW>
 __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, int pt, int lane, int c0, int kmax,
                               const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
                               unsigned char *sA, TcSlotMeta *s_meta, const TcBars &bars, const unsigned *s_thr,
-                              unsigned sshift) {
+                              unsigned sshift, int a_from, int a_to) {
     const int r0 = pt * d.na;
     int e[kTcMaxPart];
-    int a = (g - c0) & 1;  // first tile of this group
-    if (a >= d.na) return 0;
+    int a = a_from + ((g - c0 - a_from) & 1);  // this group's first tile in [a_from, a_to)
+    a_to = min(a_to, d.na);
+    if (a >= a_to) return 0;
     tc_unrank<H>(d.hbase0 + min(r0 + a, d.nheads - 1), d.b, binom, BKs, e);
     const size_t a_slot = size_t(kTcHeads) * kmax;
     int wrote = 0;
-    for (; a < d.na; a += 2) {
+    for (; a < a_to; a += 2) {
         if (wrote > 0) {
             if (r0 + a - 1 < d.nheads) tc_succ<H>(e);
             if (r0 + a < d.nheads) tc_succ<H>(e);
@@ -252,9 +267,17 @@ struct TcGaps {
 #define TCG_ARGS(k)
 #endif
 
+// The MMA warp's inner loop: one head tile (descriptor aT) against the chunk's nbt tail tiles,
+// one TMEM stage each. Tail tile nb is ring fill Fc + nb (slot bslot0 + nb mod nsb); `release`
+// (the chunk's last head tile) hands each slot back (sempty) as soon as its stage's MMAs finish.
+// Kept lean: the tensor pipe takes about one MMA ahead, so every cycle the issuer spends
+// between MMAs is a bubble.
 template <int KT>
-__device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t b_tile16, int nbt, uint32_t tbase,
-                                              uint32_t idesc, uint32_t &st, uint32_t &tpar, const TcBars &bars TCP_PARAMS TCG_PARAMS) {
+__device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t b_tile16, int nbt, int bslot0,
+                                              uint32_t bpar0, int nsb, bool release, uint32_t tbase, uint32_t idesc,
+                                              uint32_t &st, uint32_t &tpar, const TcBars &bars TCP_PARAMS TCG_PARAMS) {
+    int slot = bslot0;
+    uint32_t bpar = bpar0;
     for (int nb = 0; nb < nbt; nb++) {
 #ifdef SDB_TC_GAPS
         const unsigned long long w0 = clock64();
@@ -262,6 +285,7 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t
         TCP_BEGIN
         tc::mbar_wait_a(bar_at(bars.tempty, st), tpar ^ 1);
         TCP_END(3)
+        tc::mbar_wait_a(bar_at(bars.bfull, slot), bpar);  // immediate unless the chunk is still being written
 #ifdef SDB_TC_GAPS
         {
             const unsigned long long now = clock64();
@@ -276,7 +300,7 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t
 #endif
         TCP_BEGIN
         tc::fence_after();
-        const uint64_t bT = bU + uint64_t(nb) * b_tile16;
+        const uint64_t bT = bD + uint64_t(slot) * b_tile16;
 #ifndef SDB_TC_NOMMA  // pipeline experiments: the MMAs skipped
 #pragma unroll
         for (int k = 0; k < KT; k++)
@@ -284,9 +308,14 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bU, uint32_t
                              idesc, k > 0);
 #endif
         tc::commit_elect_a(bar_at(bars.tfull, st));
+        if (release) tc::commit_elect_a(bar_at(bars.bempty, slot));
         TCP_END(4)
         st ^= 1u;
         tpar ^= st == 0 ? 1u : 0u;
+        if (++slot == nsb) {
+            slot = 0;
+            bpar ^= 1u;
+        }
     }
 }
 
@@ -333,7 +362,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             tc::mbar_init(&sh.aempty[s], 1 + 32 * kTcEpiWarps);   // MMA commit + every epilogue thread (read the meta)
 #endif
         }
-        for (int s = 0; s < 2; s++) {
+        for (int s = 0; s < kTcMaxBSlots; s++) {
             tc::mbar_init(&sh.bfull[s], kTcProdWarps);
             tc::mbar_init(&sh.bempty[s], 1);
         }
@@ -352,7 +381,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     const uint32_t tbase = s_tbase;
     const TcBars bars(sh);
     const size_t a_slot = size_t(kTcHeads) * kmax;           // bytes per head tile
-    const size_t b_buf = size_t(tp.nbt) * kTcTileN * kmax;   // bytes per tail buffer
+    const int nsb = tp.nbt + 1;                              // B ring slots (tail tiles)
 
     if (warp == 0) {
         // ------------------------------------------------------------ MMA issuer: the whole
@@ -364,12 +393,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             const uint64_t aD = tc::sdesc(tc::smem_u32(sA), kTcHeads * 16, 128);
             const uint64_t bD = tc::sdesc(tc::smem_u32(sB), kTcTileN * 16, 128);
             const uint32_t b_tile16 = uint32_t((size_t(kTcTileN) * kmax) >> 4);
-            int ts = 0, cur_bb = -1;
+            int ts = 0;
+            unsigned long long Fc = 0, Fn = 0;  // B ring: the current chunk's first fill, the next free fill
             uint32_t st = 0, tpar = 0;  // next TMEM stage and the parity its tempty wait expects
 #ifdef SDB_TC_GAPS
             TcGaps gaps;
 #endif
-            int uses[2] = {0, 0}, c = 0;
+            int c = 0;
             TCP_DECL
             const unsigned long long tcp_start = clock64();
             for (int u = 0;; u++) {
@@ -394,15 +424,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     break;
                 }
                 if (d.restage) {
-                    if (cur_bb >= 0) tc::commit_elect_a(bar_at(bars.bempty, cur_bb));  // old buffer free once its MMAs finish
-                    cur_bb = d.bb;
-                    TCP_BEGIN
-                    tc::mbar_wait_a(bar_at(bars.bfull, cur_bb), uses[cur_bb] & 1);
-                    TCP_END(1)
-                    uses[cur_bb]++;
+                    Fc = Fn;
+                    Fn += unsigned(d.nbt);
                 }
                 const int KT = s_gam[d.j].K / 32;
-                const uint64_t bU = bD + uint64_t((size_t(cur_bb) * b_buf) >> 4);
+                const int bslot0 = int(Fc % unsigned(nsb));
+                const uint32_t bpar0 = uint32_t((Fc / unsigned(nsb)) & 1u);
                 for (int a = 0; a < d.na; a++, c++) {
                     const int s = tc_slot(c);
 #ifndef SDB_TC_MMA_NOAFULL
@@ -420,11 +447,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     tc::fence_after();
 #endif
                     const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
+                    const bool rel = d.chunk_last && a == d.na - 1;  // the chunk's last head tile frees its slots
                     switch (KT) {
-                        case 1: tc_mma_stages<1>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                        case 2: tc_mma_stages<2>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                        case 3: tc_mma_stages<3>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                        default: tc_mma_stages<4>(aT, bU, b_tile16, d.nbt, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        case 1: tc_mma_stages<1>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        case 2: tc_mma_stages<2>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        case 3: tc_mma_stages<3>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
+                        default: tc_mma_stages<4>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
                     }
                     ts += d.nbt;
                     tc::commit_elect_a(bar_at(bars.aempty, s));
@@ -559,20 +587,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             const unsigned long long local_units =
                 (tl.unit_total + tl.shard_world - 1 - tl.shard_rank) / tl.shard_world;
             constexpr int kHB = kTcHeads * kTcUnitTiles;  // heads per unit
-            int cur_bb = -1, sj = -1, sb = -1;
+            int sj = -1, sb = -1;
             unsigned long long st0 = 0, claim = 0, claim_end = 0, seen = 0, visited = 0, skipped = 0;
             int lo = 0;  // (Gamma, b) index of the previous unit: units of a run mostly share it
-            for (int u = 0;; u++) {
-                TcUnitDesc d{};
-                if (claim == claim_end) {
-                    const unsigned long long run = seen + 4ull * 4 * gridDim.x < local_units ? 4ull : 1ull;
-                    claim = atomicAdd(tl.counter, run);
-                    claim_end = claim + run;
-                    seen = claim_end;
-                }
-                const unsigned long long unit = (claim++) * tl.shard_world + tl.shard_rank;
-                d.end = unit >= tl.unit_total;
-                if (!d.end) {
+            // the next unit in dispensing order (skipping what the early exit leaves out)
+            auto next_unit = [&](TcUnitDesc &d) {
+                for (;;) {
+                    d = TcUnitDesc{};
+                    if (claim == claim_end) {
+                        const unsigned long long run = seen + 4ull * 4 * gridDim.x < local_units ? 4ull : 1ull;
+                        claim = atomicAdd(tl.counter, run);
+                        claim_end = claim + run;
+                        seen = claim_end;
+                    }
+                    const unsigned long long unit = (claim++) * tl.shard_world + tl.shard_rank;
+                    d.end = unit >= tl.unit_total;
+                    if (d.end) return;
                     if (!(s_cum[lo] <= unit && unit < s_cum[lo + 1])) {
                         int l = 0, hi = G * tl.nb - 1;
                         while (l < hi) {
@@ -599,21 +629,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     if ((unsigned long long)d.j > (early_key(p, tl.lprev) >> kKeyRankBits)) {
                         // mid-level early exit: a later Gamma's keys all exceed the best one
                         skipped += (unsigned long long)d.nheads * (unsigned long long)d.ntails;
-                        u--;  // nothing published for this claim
                         continue;
                     }
                     d.restage = d.j != sj || b != sb || d.t0 != st0;
-                    if (d.restage) cur_bb = cur_bb < 0 ? 0 : cur_bb ^ 1;
-                    d.bb = cur_bb;
                     sj = d.j;
                     sb = b;
                     st0 = d.t0;
                     visited += (unsigned long long)d.nheads * (unsigned long long)d.ntails;
+                    return;
                 }
+            };
+            // one unit of lookahead: a unit is published once the next one is known, so it can
+            // say whether its tail chunk ends with it (the MMA then frees the B ring slots tile by
+            // tile during the unit's last head tile)
+            TcUnitDesc pend;
+            next_unit(pend);
+            for (int u = 0;; u++) {
+                TcUnitDesc nd{};
+                if (pend.end) nd.end = 1; else next_unit(nd);
+                pend.chunk_last = nd.end || nd.restage;
                 tc::mbar_wait_a(bar_at(bars.uqempty, u % kTcUnitQ), ((u / kTcUnitQ) & 1) ^ 1);
-                s_uq[u % kTcUnitQ] = d;
+                s_uq[u % kTcUnitQ] = pend;
                 tc::mbar_arrive_a(bar_at(bars.uqfull, u % kTcUnitQ));
-                if (d.end) break;
+                if (pend.end) break;
+                pend = nd;
             }
             s_visited = visited;
             if (skipped) atomicAdd(&p.state->skipped, skipped);
@@ -626,7 +665,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const int pt = 32 * (pw & 3) + lane;       // head row
         const int pq = 32 * pw + lane;             // tail thread index (0..255)
         int c0 = 0;                                // kernel-wide index of the unit's first head tile
-        int fills[2] = {0, 0};
+        unsigned long long Fc = 0, Fn = 0;         // B ring: the current chunk's first fill, the next free fill
         for (int u = 0;; u++) {
             tc::mbar_wait_a(bar_at(bars.uqfull, u % kTcUnitQ), (u / kTcUnitQ) & 1);
             const TcUnitDesc d = s_uq[u % kTcUnitQ];
@@ -637,25 +676,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             const uint32_t *sg = s_sign + size_t(d.j) * N * KW;
             const short *mk = s_mask + d.j * N;
             if (d.restage) {
-                const int bb = d.bb;
-                if (lane == 0) tc::mbar_wait_a(bar_at(bars.bempty, bb), (fills[bb] & 1) ^ 1);
-                fills[bb]++;
-                __syncwarp();
-                unsigned char *buf = sB + size_t(bb) * b_buf;
-#ifndef SDB_TC_NOPROD  // pipeline experiments: the producers only signal
-                switch (tl.t - 1) {
-#define SDB_TC_TAILS(m) \
-    case m: tc_write_tails<m, KW>(d, gm, pq, N, kmax, sg, mk, s_binom, BKs, buf); break;
-                    SDB_TC_TAILS(0) SDB_TC_TAILS(1) SDB_TC_TAILS(2) SDB_TC_TAILS(3) SDB_TC_TAILS(4)
-                    SDB_TC_TAILS(5) SDB_TC_TAILS(6) SDB_TC_TAILS(7) SDB_TC_TAILS(8)
-#undef SDB_TC_TAILS
-                }
-#endif
-                tc::fence_async_smem();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive_a(bar_at(bars.bfull, bb));
+                Fc = Fn;
+                Fn += unsigned(d.nbt);
             }
 #ifdef SDB_TC_NOPROD
+            if (d.restage)
+                for (int r = 0; r < d.nbt; r++) {
+                    const unsigned long long F = Fc + unsigned(r);
+                    const int slot = int(F % unsigned(nsb));
+                    if (lane == 0) tc::mbar_wait_a(bar_at(bars.bempty, slot), uint32_t((F / unsigned(nsb)) & 1u) ^ 1u);
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive_a(bar_at(bars.bfull, slot));
+                }
             for (int a = (g - c0) & 1; a < d.na; a += 2) {
                 const int s = tc_slot(c0 + a);
                 if (lane == 0) tc::mbar_wait_a(bar_at(bars.aempty, s), tc_slot_par(c0 + a) ^ 1);
@@ -663,15 +695,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 if (lane == 0) tc::mbar_arrive_a(bar_at(bars.afull, s));
             }
 #else
-            switch (tl.h) {
-#define SDB_TC_HEADS(m) \
-    case m:                                                                                                \
-        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, bars, &s_thr, sshift); \
+#define SDB_TC_HEADS(from, to)                                                                                \
+    switch (tl.h) {                                                                                           \
+        SDB_TC_HEADS_CASE(1, from, to) SDB_TC_HEADS_CASE(2, from, to) SDB_TC_HEADS_CASE(3, from, to)            \
+        SDB_TC_HEADS_CASE(4, from, to) SDB_TC_HEADS_CASE(5, from, to) SDB_TC_HEADS_CASE(6, from, to)            \
+        SDB_TC_HEADS_CASE(7, from, to) SDB_TC_HEADS_CASE(8, from, to)                                           \
+    }
+#define SDB_TC_HEADS_CASE(m, from, to)                                                                        \
+    case m:                                                                                                   \
+        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, bars, &s_thr, sshift, \
+                              from, to);                                                                      \
         break;
-                SDB_TC_HEADS(1) SDB_TC_HEADS(2) SDB_TC_HEADS(3) SDB_TC_HEADS(4)
-                SDB_TC_HEADS(5) SDB_TC_HEADS(6) SDB_TC_HEADS(7) SDB_TC_HEADS(8)
-#undef SDB_TC_HEADS
+            int a_from = 0;
+            if (d.restage) {
+                // the new chunk's first head tiles go first (the MMA needs them and tail tile 0 to
+                // start); tail tiles follow, each as soon as the ring slot it takes is released
+                SDB_TC_HEADS(0, 2)
+                a_from = 2;
+                switch (tl.t - 1) {
+#define SDB_TC_TAILS(m) \
+    case m: tc_write_tails<m, KW>(d, gm, pq, lane, N, kmax, sg, mk, s_binom, BKs, sB, Fc, nsb, bars); break;
+                    SDB_TC_TAILS(0) SDB_TC_TAILS(1) SDB_TC_TAILS(2) SDB_TC_TAILS(3) SDB_TC_TAILS(4)
+                    SDB_TC_TAILS(5) SDB_TC_TAILS(6) SDB_TC_TAILS(7) SDB_TC_TAILS(8)
+#undef SDB_TC_TAILS
+                }
             }
+            SDB_TC_HEADS(a_from, d.na)
+#undef SDB_TC_HEADS
+#undef SDB_TC_HEADS_CASE
 #endif
             c0 += d.na;
         }
