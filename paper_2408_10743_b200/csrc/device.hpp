@@ -213,7 +213,10 @@ constexpr int kTcMaxPart = 8;      // h <= 8 and t - 1 <= 8 (element lists live 
 constexpr int kTcTileN = 256;      // tails per B tile = MMA N = TMEM columns per stage
 constexpr int kTcStages = 2;       // TMEM stages (512 columns)
 constexpr int kTcProdWarps = 8;    // producer warps: two groups of 4 (alternate head tiles; 128 rows each)
-constexpr int kTcSlots = 4;        // head tiles in flight
+#ifndef SDB_TC_SLOTS
+#define SDB_TC_SLOTS 4
+#endif
+constexpr int kTcSlots = SDB_TC_SLOTS;  // head tiles in flight (A ring)
 constexpr int kTcUnitQ = 8;        // unit descriptors in flight
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcThreads = 32 * (1 + kTcEpiWarps + 1 + kTcProdWarps);

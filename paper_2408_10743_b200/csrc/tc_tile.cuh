@@ -262,9 +262,13 @@ struct TcGaps {
 };
 #define TCG_PARAMS , TcGaps &gp, int kind0
 #define TCG_ARGS(k) , gaps, (k)
+#define TCGU_PARAMS , TcGaps &gaps
+#define TCGU_ARGS , gaps
 #else
 #define TCG_PARAMS
 #define TCG_ARGS(k)
+#define TCGU_PARAMS
+#define TCGU_ARGS
 #endif
 
 // The MMA warp's inner loop: one head tile (descriptor aT) against the chunk's nbt tail tiles,
@@ -274,8 +278,9 @@ struct TcGaps {
 // between MMAs is a bubble.
 template <int KT>
 __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t b_tile16, int nbt, int bslot0,
-                                              uint32_t bpar0, int nsb, bool release, uint32_t tbase, uint32_t idesc,
-                                              uint32_t &st, uint32_t &tpar, const TcBars &bars TCP_PARAMS TCG_PARAMS) {
+                                              uint32_t bpar0, int nsb, bool bwait, bool release, uint32_t tbase,
+                                              uint32_t idesc, uint32_t &st, uint32_t &tpar,
+                                              const TcBars &bars TCP_PARAMS TCG_PARAMS) {
     int slot = bslot0;
     uint32_t bpar = bpar0;
     for (int nb = 0; nb < nbt; nb++) {
@@ -285,7 +290,7 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t
         TCP_BEGIN
         tc::mbar_wait_a(bar_at(bars.tempty, st), tpar ^ 1);
         TCP_END(3)
-        tc::mbar_wait_a(bar_at(bars.bfull, slot), bpar);  // immediate unless the chunk is still being written
+        if (bwait) tc::mbar_wait_a(bar_at(bars.bfull, slot), bpar);  // a chunk's first head tile only
 #ifdef SDB_TC_GAPS
         {
             const unsigned long long now = clock64();
@@ -316,6 +321,33 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t
             slot = 0;
             bpar ^= 1u;
         }
+    }
+}
+
+// All head tiles of one unit (KT fixed per Gamma: one dispatch per unit, not per tile).
+template <int KT>
+__device__ __forceinline__ void tc_mma_unit(const TcUnitDesc &d, int &c, uint64_t aD, size_t a_slot, uint64_t bD,
+                                            uint32_t b_tile16, int bslot0, uint32_t bpar0, int nsb, uint32_t tbase,
+                                            uint32_t idesc, uint32_t &st, uint32_t &tpar,
+                                            const TcBars &bars TCP_PARAMS TCGU_PARAMS) {
+    for (int a = 0; a < d.na; a++, c++) {
+        const int s = tc_slot(c);
+#ifndef SDB_TC_MMA_NOAFULL
+#ifdef SDB_TC_GAPS
+        const unsigned long long aw0 = clock64();
+#endif
+        TCP_BEGIN
+        tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
+        TCP_END(2)
+#ifdef SDB_TC_GAPS
+        gaps.afw += clock64() - aw0;
+#endif
+#endif
+        const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
+        // the tail tiles were written for the chunk's first head tile; its last frees the slots
+        tc_mma_stages<KT>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, d.restage && a == 0,
+                          d.chunk_last && a == d.na - 1, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1));
+        tc::commit_elect_a(bar_at(bars.aempty, s));
     }
 }
 
@@ -430,33 +462,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 const int KT = s_gam[d.j].K / 32;
                 const int bslot0 = int(Fc % unsigned(nsb));
                 const uint32_t bpar0 = uint32_t((Fc / unsigned(nsb)) & 1u);
-                for (int a = 0; a < d.na; a++, c++) {
-                    const int s = tc_slot(c);
-#ifndef SDB_TC_MMA_NOAFULL
-#ifdef SDB_TC_GAPS
-                    const unsigned long long aw0 = clock64();
-#endif
-                    TCP_BEGIN
-                    tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
-                    TCP_END(2)
-#ifdef SDB_TC_GAPS
-                    gaps.afw += clock64() - aw0;
-#endif
-#endif
-#ifdef SDB_TC_FENCE_AFULL  // A/B: the producers' fence.proxy.async + the mbarrier already order the smem writes
-                    tc::fence_after();
-#endif
-                    const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
-                    const bool rel = d.chunk_last && a == d.na - 1;  // the chunk's last head tile frees its slots
-                    switch (KT) {
-                        case 1: tc_mma_stages<1>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                        case 2: tc_mma_stages<2>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                        case 3: tc_mma_stages<3>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                        default: tc_mma_stages<4>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, rel, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1)); break;
-                    }
-                    ts += d.nbt;
-                    tc::commit_elect_a(bar_at(bars.aempty, s));
+                switch (KT) {
+#define SDB_TC_UNIT(k)                                                                                     \
+    case k:                                                                                                \
+        tc_mma_unit<k>(d, c, aD, a_slot, bD, b_tile16, bslot0, bpar0, nsb, tbase, idesc, st, tpar, bars TCP_ARGS \
+                       TCGU_ARGS);                                                                         \
+        break;
+                    SDB_TC_UNIT(1) SDB_TC_UNIT(2) SDB_TC_UNIT(3)
+                    default: tc_mma_unit<4>(d, c, aD, a_slot, bD, b_tile16, bslot0, bpar0, nsb, tbase, idesc, st, tpar,
+                                            bars TCP_ARGS TCGU_ARGS);
+                        break;
+#undef SDB_TC_UNIT
                 }
+                ts += d.na * d.nbt;
             }
         }
     } else if (warp <= kTcEpiWarps) {
