@@ -47,15 +47,26 @@ ColumnSet columns_of(const BitMat &m, int N, int n, bool image) {
     c.N = N;
     c.words = (N + 63) / 64;
     c.bits.assign(size_t(3) * n * c.words, 0);
-    for (int r = 0; r < m.rows && r < N; r++)
-        for (int s = 0; s < n; s++) {
-            const bool a = m.get(r, s), b = m.get(r, n + s);
-            const bool ab = image ? m.get(r, 2 * n + s) : (a != b);
-            const uint64_t bit = uint64_t(1) << (r & 63);
-            if (a) c.bits[(size_t(0) * n + s) * c.words + (r >> 6)] |= bit;
-            if (b) c.bits[(size_t(1) * n + s) * c.words + (r >> 6)] |= bit;
-            if (ab) c.bits[(size_t(2) * n + s) * c.words + (r >> 6)] |= bit;
+    // transpose by visiting set bits only: column (type, s) of the a, b and a^b blocks
+    for (int r = 0; r < m.rows && r < N; r++) {
+        const uint64_t *row = m.row(r);
+        const uint64_t bit = uint64_t(1) << (r & 63);
+        const int ncols = image ? 3 * n : 2 * n;
+        for (int w = 0; w * 64 < ncols; w++) {
+            uint64_t x = row[w];
+            if (64 * w + 64 > ncols) x &= (uint64_t(1) << (ncols - 64 * w)) - 1;
+            while (x) {
+                const int col = 64 * w + __builtin_ctzll(x);
+                x &= x - 1;
+                c.bits[size_t(col) * c.words + (r >> 6)] |= bit;  // col = type * n + s
+            }
         }
+    }
+    if (!image)  // the a^b column from a and b
+        for (int s = 0; s < n; s++)
+            for (int i = 0; i < c.words; i++)
+                c.bits[(size_t(2) * n + s) * c.words + i] =
+                    c.bits[size_t(s) * c.words + i] ^ c.bits[(size_t(n) + s) * c.words + i];
     return c;
 }
 
@@ -71,8 +82,10 @@ TcEncoding tc_encode(const std::vector<const BitMat *> &mats, int N, int n, bool
     };
     std::vector<std::vector<Coord>> c1(static_cast<size_t>(G)), c3(static_cast<size_t>(G));
     enc.kmax = 32;
+    std::vector<ColumnSet> cols(static_cast<size_t>(G));
+    for (int j = 0; j < G; j++) cols[size_t(j)] = columns_of(*mats[size_t(j)], N, n, image);
     for (int j = 0; j < G; j++) {
-        const ColumnSet cs = columns_of(*mats[size_t(j)], N, n, image);
+        const ColumnSet &cs = cols[size_t(j)];
         auto col = [&](int type, int s) { return cs.bits.data() + (size_t(type) * n + s) * cs.words; };
         auto weight = [&](int type, int s) {
             int w = 0;
@@ -144,15 +157,17 @@ TcEncoding tc_encode(const std::vector<const BitMat *> &mats, int N, int n, bool
     enc.sign.assign(size_t(G) * N * enc.kw, 0);
     enc.mask.assign(size_t(G) * N, -1);
     for (int j = 0; j < G; j++) {
-        const ColumnSet cs = columns_of(*mats[size_t(j)], N, n, image);
+        const ColumnSet &cs = cols[size_t(j)];
         const std::vector<Coord> &L = layout[size_t(j)];
         for (int k = 0; k < int(L.size()); k++) {
             const Coord &c = L[size_t(k)];
             if (c.type < 0) continue;
             const uint64_t *colw = cs.bits.data() + (size_t(c.type) * n + c.sym) * cs.words;
-            for (int r = 0; r < N; r++)
-                if ((colw[r >> 6] >> (r & 63)) & 1)
-                    enc.sign[(size_t(j) * N + r) * enc.kw + k / 32] |= uint32_t(1) << coord_bit(k);
+            for (int i = 0; i < cs.words; i++)
+                for (uint64_t x = colw[i]; x; x &= x - 1) {
+                    const int r = 64 * i + __builtin_ctzll(x);
+                    if (r < N) enc.sign[(size_t(j) * N + r) * enc.kw + k / 32] |= uint32_t(1) << coord_bit(k);
+                }
             if (c.mask_row >= 0) enc.mask[size_t(j) * N + c.mask_row] = short(k);
         }
     }
