@@ -241,10 +241,13 @@ struct TcUnitDesc {
     unsigned long long hbase0, t0;
     int j, b, nheads, ntails, nbt, na, chunk_last, restage, end, pad;  // chunk_last: the next unit restages
 };
-struct TcSlotMeta {
-    short ch[kTcHeads];    // per head row: alpha * |S_h ∩ mask rows|
-    short tenc[kTcHeads];  // per head row: the threshold T folded into its kt bytes
-};
+// What the MMA warp needs of a unit, in one word (TcUnitDesc::pad) it makes warp-uniform with
+// one redux.sync: na | nbt << 8 | K / 32 << 16 | flags.
+constexpr unsigned kTcWordRestage = 1u << 20, kTcWordChunkLast = 1u << 21, kTcWordEnd = 1u << 22;
+SDB_HD inline unsigned tc_unit_word(const TcUnitDesc &d, int kt) {
+    return unsigned(d.na) | unsigned(d.nbt) << 8 | unsigned(kt) << 16 | (d.restage ? kTcWordRestage : 0u) |
+           (d.chunk_last ? kTcWordChunkLast : 0u) | (d.end ? kTcWordEnd : 0u);
+}
 // -(T + 1) as the head's two threshold bytes (r at kt, q at kt + 1; the tail holds 1, 16),
 // clamped to what they can carry: a larger T only sends more pairs down the exact path, a
 // T below -2048 passes nothing either way (|val| <= 2 K)
@@ -263,7 +266,7 @@ struct TcPlan {
     const TcGammaDev *gam;    // [G]
 };
 struct TcSmem {
-    size_t a, b, sign, mask, rows, binom, meta, uq, gam, cum, total;
+    size_t a, b, sign, mask, rows, binom, uq, gam, cum, total;
 };
 SDB_HD inline TcSmem tc_smem_layout(int G, int N, int W, int kmax, int kw, int nbt, int BKs) {
     TcSmem L{};
@@ -273,8 +276,7 @@ SDB_HD inline TcSmem tc_smem_layout(int G, int N, int W, int kmax, int kw, int n
     L.mask = align16(L.sign + size_t(G) * N * kw * 4);
     L.rows = align16(L.mask + size_t(G) * N * 2);
     L.binom = align16(L.rows + size_t(G) * N * 2 * W * 4);
-    L.meta = align16(L.binom + size_t(N + 1) * BKs * 8);
-    L.uq = align16(L.meta + size_t(kTcSlots) * sizeof(TcSlotMeta));
+    L.uq = align16(L.binom + size_t(N + 1) * BKs * 8);
     L.gam = align16(L.uq + size_t(kTcUnitQ) * sizeof(TcUnitDesc));
     L.cum = align16(L.gam + size_t(G) * sizeof(TcGammaDev));       // the level's unit table
     L.total = align16(L.cum + (size_t(G) * (N + 1) + 1) * 8);

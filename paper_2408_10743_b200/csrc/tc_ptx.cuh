@@ -131,6 +131,21 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
         "r"(parity), "r"(0x989680)
         : "memory");
 }
+// The same wait from a converged warp, with a warp-uniform exit (vote.all over the lanes'
+// try_wait results): ptxas then sees uniform control flow around the wait and keeps the
+// caller's warp-uniform state (descriptors, barrier addresses, counters) in uniform registers.
+__device__ __forceinline__ void mbar_wait_u(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity), "r"(0x989680)
+            : "memory");
+    } while (!__all_sync(0xffffffffu, ok));
+}
 __device__ __forceinline__ void commit_elect_a(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -138,6 +153,72 @@ __device__ __forceinline__ void commit_elect_a(uint32_t bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
         : "memory");
 }
+
+// One TMEM stage of the MMA warp as a single block, from a converged warp: wait for the stage's
+// tempty phase (and, when `bwait`, for the tail tile's bfull phase), then the elected lane issues
+// the KT MMAs of the stage (K = 32 each; the operand descriptors advance by a_step / b_step per
+// K step), commits them to `tfull` and, when `release`, to the tail slot's `bempty`. Everything
+// the MMAs need is an input of the block, so it is computed before the wait and the path from
+// the barrier flip to the first UTCIMMA holds no address arithmetic.
+#define SDB_MMA_STAGE_HEAD                                                       \
+    "{\n\t"                                                                      \
+    ".reg .pred p, e, bw, rel, pf, pt;\n\t"                                      \
+    ".reg .b64 a1, a2, a3, b1, b2, b3, as, bs;\n\t"                              \
+    "setp.ne.b32 bw, %4, 0;\n\t"                                                 \
+    "setp.ne.b32 rel, %13, 0;\n\t"                                               \
+    "setp.ne.b32 pf, 0, 0;\n\t"                                                  \
+    "setp.eq.b32 pt, 0, 0;\n\t"                                                  \
+    "cvt.u64.u32 as, %8;\n\t"                                                    \
+    "cvt.u64.u32 bs, %9;\n\t"                                                    \
+    "add.u64 a1, %6, as;\n\t"                                                    \
+    "add.u64 b1, %7, bs;\n\t"                                                    \
+    "add.u64 a2, a1, as;\n\t"                                                    \
+    "add.u64 b2, b1, bs;\n\t"                                                    \
+    "add.u64 a3, a2, as;\n\t"                                                    \
+    "add.u64 b3, b2, bs;\n\t"                                                    \
+    "elect.sync _|e, 0xffffffff;\n\t"                                            \
+    "and.pred rel, rel, e;\n"                                                    \
+    "WT_%=:\n\t"                                                                 \
+    "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %14;\n\t"             \
+    "@!p bra WT_%=;\n\t"                                                         \
+    "@!bw bra GO_%=;\n"                                                          \
+    "WB_%=:\n\t"                                                                 \
+    "mbarrier.try_wait.parity.shared::cta.b64 p, [%2], %3, %14;\n\t"             \
+    "@!p bra WB_%=;\n"                                                           \
+    "GO_%=:\n\t"                                                                 \
+    "tcgen05.fence::after_thread_sync;\n\t"                                      \
+    "@e tcgen05.mma.cta_group::1.kind::i8 [%5], %6, %7, %10, pf;\n\t"
+#define SDB_MMA_STAGE_K(a, b) "@e tcgen05.mma.cta_group::1.kind::i8 [%5], " a ", " b ", %10, pt;\n\t"
+#define SDB_MMA_STAGE_TAIL                                                                        \
+    "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t"         \
+    "@rel tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t"       \
+    "}\n"
+#define SDB_MMA_STAGE_OPS                                                                                         \
+    ::"r"(tempty), "r"(tpar), "r"(bfull), "r"(bpar), "r"(uint32_t(bwait)), "r"(d_tmem), "l"(adesc), "l"(bdesc),     \
+        "r"(a_step), "r"(b_step), "r"(idesc), "r"(tfull), "r"(bempty), "r"(uint32_t(release)), "r"(0x989680)        \
+        : "memory"
+template <int KT>
+__device__ __forceinline__ void mma_stage(uint32_t tempty, uint32_t tpar, uint32_t bfull, uint32_t bpar, bool bwait,
+                                          uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t a_step,
+                                          uint32_t b_step, uint32_t idesc, uint32_t tfull, uint32_t bempty,
+                                          bool release) {
+    static_assert(KT >= 1 && KT <= 4, "K steps per stage");
+    if constexpr (KT == 1) {
+        asm volatile(SDB_MMA_STAGE_HEAD SDB_MMA_STAGE_TAIL SDB_MMA_STAGE_OPS);
+    } else if constexpr (KT == 2) {
+        asm volatile(SDB_MMA_STAGE_HEAD SDB_MMA_STAGE_K("a1", "b1") SDB_MMA_STAGE_TAIL SDB_MMA_STAGE_OPS);
+    } else if constexpr (KT == 3) {
+        asm volatile(SDB_MMA_STAGE_HEAD SDB_MMA_STAGE_K("a1", "b1") SDB_MMA_STAGE_K("a2", "b2")
+                         SDB_MMA_STAGE_TAIL SDB_MMA_STAGE_OPS);
+    } else {
+        asm volatile(SDB_MMA_STAGE_HEAD SDB_MMA_STAGE_K("a1", "b1") SDB_MMA_STAGE_K("a2", "b2")
+                         SDB_MMA_STAGE_K("a3", "b3") SDB_MMA_STAGE_TAIL SDB_MMA_STAGE_OPS);
+    }
+}
+#undef SDB_MMA_STAGE_HEAD
+#undef SDB_MMA_STAGE_K
+#undef SDB_MMA_STAGE_TAIL
+#undef SDB_MMA_STAGE_OPS
 
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

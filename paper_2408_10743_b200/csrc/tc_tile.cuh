@@ -113,7 +113,15 @@ __device__ __forceinline__ void tc_gather(const uint32_t *sg, const short *mk, i
 __device__ __forceinline__ int tc_slot(int c) { return c % kTcSlots; }
 __device__ __forceinline__ uint32_t tc_slot_par(int c) { return (c / kTcSlots) & 1; }
 
+#ifdef SDB_TC_LAT
+// signalling latencies between the MMA warp and the epilogue (variant builds): SM clock stamps
+// through shared memory; block 0 prints the averages
+__device__ unsigned long long g_tc_lat[8];
+#endif
 struct TcShared {
+#ifdef SDB_TC_LAT
+    volatile long long lat_commit[kTcStages], lat_arrive[kTcStages], lat_acc[8];
+#endif
     uint64_t uqfull[kTcUnitQ], uqempty[kTcUnitQ], afull[kTcSlots], aempty[kTcSlots], bfull[kTcMaxBSlots],
         bempty[kTcMaxBSlots],
         tfull[kTcStages], tempty[kTcStages];
@@ -186,7 +194,7 @@ __device__ void tc_write_tails(const TcUnitDesc &d, const TcGammaDev &gm, int pq
 template <int H, int KW>
 __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, int pt, int lane, int c0, int kmax,
                               const uint32_t *sg, const short *mk, const unsigned long long *binom, int BKs,
-                              unsigned char *sA, TcSlotMeta *s_meta, const TcBars &bars, const unsigned *s_thr,
+                              unsigned char *sA, const TcBars &bars, const unsigned *s_thr,
                               unsigned sshift, int a_from, int a_to) {
     const int r0 = pt * d.na;
     int e[kTcMaxPart];
@@ -226,8 +234,6 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
         tc_threshold_bytes(T, tr, tq);
         tile[tc::kmajor_off(kTcHeads, pt, gm.kt)] = (unsigned char)tr;
         tile[tc::kmajor_off(kTcHeads, pt, gm.kt + 1)] = (unsigned char)tq;
-        s_meta[s].ch[pt] = short(chv);
-        s_meta[s].tenc[pt] = short(T);
         tc::fence_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_a(bar_at(bars.afull, s));
@@ -274,8 +280,11 @@ struct TcGaps {
 // The MMA warp's inner loop: one head tile (descriptor aT) against the chunk's nbt tail tiles,
 // one TMEM stage each. Tail tile nb is ring fill Fc + nb (slot bslot0 + nb mod nsb); `release`
 // (the chunk's last head tile) hands each slot back (sempty) as soon as its stage's MMAs finish.
-// Kept lean: the tensor pipe takes about one MMA ahead, so every cycle the issuer spends
-// between MMAs is a bubble.
+// Kept lean: every operand is warp-uniform by construction (kernel parameters, loop counters
+// and the unit's packed word taken through redux.sync), so ptxas keeps descriptors, barrier
+// addresses and loop state in uniform registers and the path from a stage's tempty wait to its
+// UTCIMMA is a handful of instructions; the tensor pipe takes about one MMA ahead, so every
+// cycle the issuer spends between MMAs is a bubble.
 template <int KT>
 __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t b_tile16, int nbt, int bslot0,
                                               uint32_t bpar0, int nsb, bool bwait, bool release, uint32_t tbase,
@@ -287,10 +296,14 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t
 #ifdef SDB_TC_GAPS
         const unsigned long long w0 = clock64();
 #endif
+        // this stage's operands, ready before the wait (tc::mma_stage)
+        const uint32_t dT = tbase + st * kTcTileN;
+        const uint64_t bT = bD + uint64_t(uint32_t(slot) * b_tile16);
+#if defined(SDB_TC_GAPS) || defined(SDB_TC_PROF) || defined(SDB_TC_NOMMA)
         TCP_BEGIN
-        tc::mbar_wait_a(bar_at(bars.tempty, st), tpar ^ 1);
+        tc::mbar_wait_u(bar_at(bars.tempty, st), tpar ^ 1);
         TCP_END(3)
-        if (bwait) tc::mbar_wait_a(bar_at(bars.bfull, slot), bpar);  // a chunk's first head tile only
+        if (bwait) tc::mbar_wait_u(bar_at(bars.bfull, slot), bpar);  // a chunk's first head tile only
 #ifdef SDB_TC_GAPS
         {
             const unsigned long long now = clock64();
@@ -305,18 +318,31 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t
 #endif
         TCP_BEGIN
         tc::fence_after();
-        const uint64_t bT = bD + uint64_t(slot) * b_tile16;
 #ifndef SDB_TC_NOMMA  // pipeline experiments: the MMAs skipped
 #pragma unroll
         for (int k = 0; k < KT; k++)
-            tc::mma_i8_elect(tbase + st * kTcTileN, aT + uint64_t(k * 2 * kTcHeads), bT + uint64_t(k * 2 * kTcTileN),
-                             idesc, k > 0);
+            tc::mma_i8_elect(dT, aT + uint64_t(k * 2 * kTcHeads), bT + uint64_t(k * 2 * kTcTileN), idesc, k > 0);
 #endif
         tc::commit_elect_a(bar_at(bars.tfull, st));
         if (release) tc::commit_elect_a(bar_at(bars.bempty, slot));
         TCP_END(4)
+#else
+        tc::mma_stage<KT>(bar_at(bars.tempty, st), tpar ^ 1, bar_at(bars.bfull, slot), bpar, bwait, dT, aT, bT,
+                          2 * kTcHeads, 2 * kTcTileN, idesc, bar_at(bars.tfull, st), bar_at(bars.bempty, slot), release);
+#ifdef SDB_TC_LAT
+        if ((threadIdx.x & 31) == 0) {
+            const long long now = clock64();
+            TcShared *shp = reinterpret_cast<TcShared *>(__cvta_shared_to_generic(bars.uqfull - offsetof(TcShared, uqfull)));
+            if (shp->lat_arrive[st] && !bwait) {
+                shp->lat_acc[0] += now - shp->lat_arrive[st];  // arrive -> next commit issue
+                shp->lat_acc[1] += 1;
+            }
+            shp->lat_commit[st] = now;
+        }
+#endif
+#endif
         st ^= 1u;
-        tpar ^= st == 0 ? 1u : 0u;
+        tpar ^= st ^ 1u;  // flips after stage 1
         if (++slot == nsb) {
             slot = 0;
             bpar ^= 1u;
@@ -326,27 +352,27 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t
 
 // All head tiles of one unit (KT fixed per Gamma: one dispatch per unit, not per tile).
 template <int KT>
-__device__ __forceinline__ void tc_mma_unit(const TcUnitDesc &d, int &c, uint64_t aD, size_t a_slot, uint64_t bD,
-                                            uint32_t b_tile16, int bslot0, uint32_t bpar0, int nsb, uint32_t tbase,
-                                            uint32_t idesc, uint32_t &st, uint32_t &tpar,
-                                            const TcBars &bars TCP_PARAMS TCGU_PARAMS) {
-    for (int a = 0; a < d.na; a++, c++) {
+__device__ __forceinline__ void tc_mma_unit(int na, int nbt, bool restage, bool chunk_last, int &c, uint64_t aD,
+                                            uint32_t a_slot16, uint64_t bD, uint32_t b_tile16, int bslot0,
+                                            uint32_t bpar0, int nsb, uint32_t tbase, uint32_t idesc, uint32_t &st,
+                                            uint32_t &tpar, const TcBars &bars TCP_PARAMS TCGU_PARAMS) {
+    for (int a = 0; a < na; a++, c++) {
         const int s = tc_slot(c);
+        const uint64_t aT = aD + uint64_t(uint32_t(s) * a_slot16);
 #ifndef SDB_TC_MMA_NOAFULL
 #ifdef SDB_TC_GAPS
         const unsigned long long aw0 = clock64();
 #endif
         TCP_BEGIN
-        tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
+        tc::mbar_wait_u(bar_at(bars.afull, s), tc_slot_par(c));
         TCP_END(2)
 #ifdef SDB_TC_GAPS
         gaps.afw += clock64() - aw0;
 #endif
 #endif
-        const uint64_t aT = aD + uint64_t((size_t(s) * a_slot) >> 4);
         // the tail tiles were written for the chunk's first head tile; its last frees the slots
-        tc_mma_stages<KT>(aT, bD, b_tile16, d.nbt, bslot0, bpar0, nsb, d.restage && a == 0,
-                          d.chunk_last && a == d.na - 1, tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1));
+        tc_mma_stages<KT>(aT, bD, b_tile16, nbt, bslot0, bpar0, nsb, restage && a == 0, chunk_last && a == na - 1,
+                          tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1));
         tc::commit_elect_a(bar_at(bars.aempty, s));
     }
 }
@@ -369,7 +395,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     short *s_mask = reinterpret_cast<short *>(smem + lay.mask);
     uint32_t *s_rows = reinterpret_cast<uint32_t *>(smem + lay.rows);
     unsigned long long *s_binom = reinterpret_cast<unsigned long long *>(smem + lay.binom);
-    TcSlotMeta *s_meta = reinterpret_cast<TcSlotMeta *>(smem + lay.meta);
     TcUnitDesc *s_uq = reinterpret_cast<TcUnitDesc *>(smem + lay.uq);
     TcGammaDev *s_gam = reinterpret_cast<TcGammaDev *>(smem + lay.gam);
     unsigned long long *s_cum = reinterpret_cast<unsigned long long *>(smem + lay.cum);
@@ -388,11 +413,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         }
         for (int s = 0; s < kTcSlots; s++) {
             tc::mbar_init(&sh.afull[s], kTcProdWarps / 2);   // the four warps of the writing group
-#ifdef SDB_TC_EPI_NOMETA
-            tc::mbar_init(&sh.aempty[s], 1);
-#else
-            tc::mbar_init(&sh.aempty[s], 1 + 32 * kTcEpiWarps);   // MMA commit + every epilogue thread (read the meta)
-#endif
+            tc::mbar_init(&sh.aempty[s], 1);                 // the MMA commit after the tile's last stage
         }
         for (int s = 0; s < kTcMaxBSlots; s++) {
             tc::mbar_init(&sh.bfull[s], kTcProdWarps);
@@ -405,6 +426,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         tc::mbar_fence_init();
         s_visited = 0;
         s_thr = start_threshold(p, tl.thr0);
+#ifdef SDB_TC_LAT
+        for (int i = 0; i < kTcStages; i++) sh.lat_commit[i] = sh.lat_arrive[i] = 0;
+        for (int i = 0; i < 8; i++) sh.lat_acc[i] = 0;
+#endif
     }
     if (warp == 0) tc::tmem_alloc(&s_tbase, 512);
     tc::fence_before();
@@ -424,9 +449,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             // operand descriptors; an offset of x bytes is + (x >> 4) on the start-address field
             const uint64_t aD = tc::sdesc(tc::smem_u32(sA), kTcHeads * 16, 128);
             const uint64_t bD = tc::sdesc(tc::smem_u32(sB), kTcTileN * 16, 128);
+            const uint32_t a_slot16 = uint32_t(a_slot >> 4);
             const uint32_t b_tile16 = uint32_t((size_t(kTcTileN) * kmax) >> 4);
+            const uint32_t tb_u = __reduce_or_sync(0xffffffffu, tbase);  // the same value, known warp-uniform
             int ts = 0;
-            unsigned long long Fc = 0, Fn = 0;  // B ring: the current chunk's first fill, the next free fill
+            // B ring: slot and phase parity of the current chunk's first fill and of the next free fill
+            int bslot_c = 0, bslot_n = 0;
+            uint32_t bpar_c = 0, bpar_n = 0;
             uint32_t st = 0, tpar = 0;  // next TMEM stage and the parity its tempty wait expects
 #ifdef SDB_TC_GAPS
             TcGaps gaps;
@@ -436,12 +465,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             const unsigned long long tcp_start = clock64();
             for (int u = 0;; u++) {
                 TCP_BEGIN
-                tc::mbar_wait_a(bar_at(bars.uqfull, u % kTcUnitQ), (u / kTcUnitQ) & 1);
+                tc::mbar_wait_u(bar_at(bars.uqfull, u % kTcUnitQ), (u / kTcUnitQ) & 1);
                 TCP_END(0)
-                const TcUnitDesc d = s_uq[u % kTcUnitQ];
+                // the unit's packed word (tc_unit_word), made warp-uniform for the compiler
+                const unsigned mw = __reduce_or_sync(0xffffffffu, unsigned(s_uq[u % kTcUnitQ].pad));
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive_a(bar_at(bars.uqempty, u % kTcUnitQ));
-                if (d.end) {
+                if (mw & kTcWordEnd) {
 #ifdef SDB_TC_GAPS
                     if (blockIdx.x == 0 && lane == 0)
                         printf("[tcgaps] afull wait avg %.1f per tile | in-tile %llu stages avg %.1f (wait %.1f) | tile start %llu avg %.1f (wait %.1f) | unit start %llu avg %.1f (wait %.1f)\n",
@@ -455,26 +485,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #endif
                     break;
                 }
-                if (d.restage) {
-                    Fc = Fn;
-                    Fn += unsigned(d.nbt);
+                const int na = int(mw & 0xffu), nbt = int((mw >> 8) & 0xffu), KT = int((mw >> 16) & 0xfu);
+                const bool restage = (mw & kTcWordRestage) != 0, chunk_last = (mw & kTcWordChunkLast) != 0;
+                if (restage) {
+                    bslot_c = bslot_n;
+                    bpar_c = bpar_n;
+                    bslot_n += nbt;  // nbt < nsb: at most one wrap
+                    if (bslot_n >= nsb) {
+                        bslot_n -= nsb;
+                        bpar_n ^= 1u;
+                    }
                 }
-                const int KT = s_gam[d.j].K / 32;
-                const int bslot0 = int(Fc % unsigned(nsb));
-                const uint32_t bpar0 = uint32_t((Fc / unsigned(nsb)) & 1u);
                 switch (KT) {
-#define SDB_TC_UNIT(k)                                                                                     \
-    case k:                                                                                                \
-        tc_mma_unit<k>(d, c, aD, a_slot, bD, b_tile16, bslot0, bpar0, nsb, tbase, idesc, st, tpar, bars TCP_ARGS \
-                       TCGU_ARGS);                                                                         \
+#define SDB_TC_UNIT(k)                                                                                       \
+    case k:                                                                                                  \
+        tc_mma_unit<k>(na, nbt, restage, chunk_last, c, aD, a_slot16, bD, b_tile16, bslot_c, bpar_c, nsb, tb_u, \
+                       idesc, st, tpar, bars TCP_ARGS TCGU_ARGS);                                            \
         break;
                     SDB_TC_UNIT(1) SDB_TC_UNIT(2) SDB_TC_UNIT(3)
-                    default: tc_mma_unit<4>(d, c, aD, a_slot, bD, b_tile16, bslot0, bpar0, nsb, tbase, idesc, st, tpar,
-                                            bars TCP_ARGS TCGU_ARGS);
+                    default: tc_mma_unit<4>(na, nbt, restage, chunk_last, c, aD, a_slot16, bD, b_tile16, bslot_c, bpar_c,
+                                            nsb, tb_u, idesc, st, tpar, bars TCP_ARGS TCGU_ARGS);
                         break;
 #undef SDB_TC_UNIT
                 }
-                ts += d.na * d.nbt;
+                ts += na * nbt;
             }
         }
     } else if (warp <= kTcEpiWarps) {
@@ -483,7 +517,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const int half = (warp - 1) >> 2;   // which 128 columns of a stage
         const int row = 32 * q + lane;      // head row of the tile = TMEM lane
         const uint32_t ta0 = tbase + (uint32_t(32 * q) << 16) + uint32_t(half * 128);  // + st * 256
-        const unsigned sshift = p.scale == 2 ? 1u : 0u;
         unsigned thrH = start_threshold(p, tl.thr0);
         unsigned s_thr_seen = thrH;  // this warp's last bound published to s_thr
         unsigned wmin_next = thrH;   // the level minimum as loaded at the previous head tile
@@ -494,6 +527,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const uint32_t tf_x = tf_st ^ bar_at(bars.tfull, 1), te_x = te_st ^ bar_at(bars.tempty, 1),
                        ta_x = ta0 ^ (ta0 + uint32_t(kTcTileN));
         int c = 0;  // head tiles consumed
+#ifdef SDB_TC_LAT
+        long long lat_r[4] = {0, 0, 0, 0};
+#endif
         TCP_DECL
         const unsigned long long tcp_start = clock64();
         for (int u = 0;; u++) {
@@ -504,12 +540,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_a(bar_at(bars.uqempty, u % kTcUnitQ));
             if (d.end) {
+#ifdef SDB_TC_LAT
+                if (blockIdx.x == 0 && lane == 0 && (warp == 1 || warp == 8) && lat_r[3] > 5000)
+                    printf("[tclat] epi warp %d: commit issue->seen %.1f | waiting %.1f | seen->release %.1f | stages %lld | mma: arrive(w8)->commit issue %.1f\n",
+                           warp, double(lat_r[0]) / lat_r[3], double(lat_r[1]) / lat_r[3], double(lat_r[2]) / lat_r[3], lat_r[3],
+                           double(sh.lat_acc[0]) / double(max(1ll, (long long)sh.lat_acc[1])));
+#endif
 #ifdef SDB_TC_PROF
                 if (blockIdx.x == 0 && lane == 0 && (warp == 1 || warp == 5)) printf("[tcprof] epi warp %d: total %llu wait_uq %llu wait_afull %llu wait_tfull %llu work %llu\n", warp, clock64() - tcp_start, tcp_acc[0], tcp_acc[1], tcp_acc[2], tcp_acc[3]);
 #endif
                 break;
             }
-            const TcGammaDev gm = s_gam[d.j];
             TileUnit un;
             un.j = d.j;
             un.b = d.b;
@@ -518,34 +559,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             un.tcount = d.ntails;
             un.pad = d.nheads;
             for (int a = 0; a < d.na; a++, c++) {
-                const int s = tc_slot(c);
-#ifdef SDB_TC_EPI_NOMETA
-                const int ch = 0, tenc = 0;
-#else
-                TCP_BEGIN
-                tc::mbar_wait_a(bar_at(bars.afull, s), tc_slot_par(c));
-                TCP_END(1)
-                const int ch = s_meta[s].ch[row], tenc = s_meta[s].tenc[row];
-                tc::mbar_arrive_a(bar_at(bars.aempty, s));
-#endif
                 const int hoff = row * d.na + a;  // this row's head: rank hbase0 + hoff
                 // other CTAs' finds: the value loaded one head tile ago (its L2 latency hidden
                 // behind that tile's stages) tightens the bound now; load the next one
                 thrH = min(thrH, wmin_next);
                 wmin_next = ld_relaxed_u32(&p.state->wmin);
-                int T = hoff < d.nheads ? gm.S * int(thrH >> sshift) - gm.C0 - ch : -32768;
                 for (int nb = 0; nb < d.nbt; nb++) {
                     TCP_BEGIN
+#ifdef SDB_TC_LAT
+                    const long long lat_enter = clock64();
+#endif
                     tc::mbar_wait_a(tf_st, tpar_e);
                     TCP_END(2)
+#ifdef SDB_TC_LAT
+                    const long long lat_seen = clock64();
+                    lat_r[0] += lat_seen - sh.lat_commit[st_e];  // commit issue -> seen
+                    lat_r[1] += lat_seen - lat_enter;             // spent waiting
+                    lat_r[3] += 1;
+#endif
                     TCP_BEGIN
                     tc::fence_after();
                     uint32_t v[64];
                     tc::ld64_pack(ta_st, v);
                     tc::ld_wait();
+#ifdef SDB_TC_LAT
+                    {
+                        const long long now = clock64();
+                        lat_r[2] += now - lat_seen;  // seen -> release
+                        if (warp == 8 && lane == 0) sh.lat_arrive[st_e] = now;
+                    }
+#endif
+                    // the accumulators are in registers: hand the TMEM stage back to the MMA
+                    // warp before looking at them (the stage's release is on the kernel's
+                    // critical path, the sign test is not)
+                    tc::fence_before();
+                    tc::mbar_arrive_a(te_st);
                     // a pair passes the folded threshold iff its 16-bit accumulator is negative:
                     // OR the packed words as a tree of 3-input ORs (depth 4; ptxas turns a plain OR
-                    // reduction into one 32-deep dependent LOP3 chain), test the two sign bits
+                    // reduction into one 32-deep dependent LOP3 chain), test the two sign bits.
+                    // The second level (8 groups of 18 columns; the last holds 2) is kept to
+                    // locate a hit.
                     uint32_t r[22];
 #pragma unroll
                     for (int i = 0; i < 21; i++) r[i] = tc::or3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
@@ -559,29 +612,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     o = 0;  // TMEM / the operands hold no real data
 #endif
                     if (__any_sync(0xffffffffu, o & 0x80008000u)) {
-                        // rare (warp-uniform: tcgen05.ld is .sync.aligned): re-read the stage
-                        // 32 columns at a time (the values stay in registers, no local copy) and
-                        // take the exact path for every pair below the folded threshold that also
-                        // passes the current one (val = acc + tenc + 1 <= T)
-                        for (int ck = 0; ck < 4; ck++) {
-                            uint32_t w[16];
-                            tc::ld16_pack(ta_st + uint32_t(32 * ck), w);
-                            tc::ld_wait();
+                        // rare: some head row of this warp has a pair below the folded threshold
+                        // in one of its column groups. The stage is already released, so the
+                        // warp recomputes: for each flagged row, its lanes take the columns of the
+                        // flagged groups through the exact path (exact weight against the
+                        // current bound, syndromes, key) — 18 candidates per flagged group.
+                        unsigned gmask = 0;
 #pragma unroll
-                            for (int i = 0; i < 32; i++) {
-                                const int acc = int(short(w[i >> 1] >> (16 * (i & 1))));
-                                if (acc >= 0 || acc + tenc + 1 > T) continue;
-                                const int y = nb * kTcTileN + half * 128 + 32 * ck + i;  // B row of the unit
+                        for (int i = 0; i < 8; i++) gmask |= (r2[i] & 0x80008000u) ? 1u << i : 0u;
+                        if (hoff >= d.nheads) gmask = 0;  // rows past the unit's heads never pass
+                        unsigned rows_hit = __ballot_sync(0xffffffffu, gmask != 0);
+                        while (rows_hit) {
+                            const int L = __ffs(rows_hit) - 1;
+                            rows_hit &= rows_hit - 1;
+                            const unsigned gmL = __shfl_sync(0xffffffffu, gmask, L);
+                            const int hoffL = __shfl_sync(0xffffffffu, hoff, L);
+#pragma unroll 1
+                            for (int i = lane; i < 128; i += 32) {
+                                if (!((gmL >> (i / 18)) & 1u)) continue;
+                                const int y = nb * kTcTileN + half * 128 + i;  // B row of the unit
                                 const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
                                                     d.ntails - 1);
-                                SDB_CHECK(tix >= 0 && tix < d.ntails && hoff < d.nheads);
-                                thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoff, tix, thrH);
-                                T = gm.S * int(thrH >> sshift) - gm.C0 - ch;
+                                SDB_CHECK(tix >= 0 && tix < d.ntails && hoffL >= 0 && hoffL < d.nheads);
+                                thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoffL, tix, thrH);
                             }
                         }
+                        thrH = __reduce_min_sync(0xffffffffu, thrH);  // the bound is global
                     }
-                    tc::fence_before();
-                    tc::mbar_arrive_a(te_st);
                     // next stage: flip the TMEM stage (and the phase parity after stage 1)
                     tf_st ^= tf_x;
                     te_st ^= te_x;
@@ -666,6 +723,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 TcUnitDesc nd{};
                 if (pend.end) nd.end = 1; else next_unit(nd);
                 pend.chunk_last = nd.end || nd.restage;
+                pend.pad = int(tc_unit_word(pend, pend.end ? 0 : s_gam[pend.j].K / 32));
                 tc::mbar_wait_a(bar_at(bars.uqempty, u % kTcUnitQ), ((u / kTcUnitQ) & 1) ^ 1);
                 s_uq[u % kTcUnitQ] = pend;
                 tc::mbar_arrive_a(bar_at(bars.uqfull, u % kTcUnitQ));
@@ -721,7 +779,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     }
 #define SDB_TC_HEADS_CASE(m, from, to)                                                                        \
     case m:                                                                                                   \
-        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, s_meta, bars, &s_thr, sshift, \
+        tc_write_heads<m, KW>(d, gm, g, pt, lane, c0, kmax, sg, mk, s_binom, BKs, sA, bars, &s_thr, sshift, \
                               from, to);                                                                      \
         break;
             int a_from = 0;

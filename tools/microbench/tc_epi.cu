@@ -59,11 +59,15 @@ __device__ __forceinline__ uint32_t or_tree(const uint32_t *v) {
 // LD: 0 = one x64 pack (128 columns), 1 = two x32 pack (64 + 64), 2 = one x64 plain (64 columns),
 //     3 = one x32 pack (64 columns: for E = 16)
 template <int LD>
-__device__ __forceinline__ uint32_t drain(uint32_t ta) {
+__device__ __forceinline__ uint32_t drain(uint32_t ta, uint32_t early_bar = 0) {
     if constexpr (LD == 0) {
         uint32_t v[64];
         ld64_pack(ta, v);
         ld_wait();
+        if (early_bar) {
+            fence_before();
+            if ((threadIdx.x & 31) == 0) mbar_arrive_a(early_bar);
+        }
         return or_tree<64>(v);
     } else if constexpr (LD == 1) {
         uint32_t v[32], w[32];
@@ -85,8 +89,35 @@ __device__ __forceinline__ uint32_t drain(uint32_t ta) {
     }
 }
 
-template <int MODE, int KT, int E, int LD, int ARR>
+// WAIT: 0 = try_wait with the suspend-time hint (the kernel's mbar_wait_a), 1 = try_wait without a
+// hint, 2 = test_wait spin
+template <int WAIT>
+__device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
+    if constexpr (WAIT == 0) {
+        mbar_wait_a(bar, parity);
+    } else if constexpr (WAIT == 1) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+    }
+}
+
+template <int MODE, int KT, int E, int LD, int ARR, int WAIT = 0, int TL = 0>
 __global__ void __launch_bounds__(32 * (1 + E), 1) epi_bench(int T, long long *cycles, int *out) {
+    __shared__ volatile long long ts_commit[2], ts_arrive[2];
+    long long lat1 = 0, lat2 = 0, wt = 0, work = 0;
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t full[2], empty[2];
     __shared__ uint32_t tbase;
@@ -116,7 +147,14 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) epi_bench(int T, long long *c
             for (int it = 0; it < T; it++) {
                 const int s = it & 1;
                 const uint32_t ph = (it >> 1) & 1;
-                mbar_wait_a(e0 + 8 * s, ph ^ 1);
+                long long w0 = 0;
+                if (TL) w0 = clock64();
+                wait_bar<WAIT>(e0 + 8 * s, ph ^ 1);
+                if (TL) {
+                    const long long now = clock64();
+                    wt += now - w0;
+                    if (it >= 2) lat2 += now - ts_arrive[s];
+                }
                 fence_after();
 #pragma unroll
                 for (int k = 0; k < KT; k++) {
@@ -124,8 +162,11 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) epi_bench(int T, long long *c
                     const uint64_t bd = sdesc(smem_u32(sB) + k * 2 * (N * 16), N * 16, 128);
                     mma_i8_elect(tb + s * N, ad, bd, id, k > 0);
                 }
+                if (TL && lane == 0) ts_commit[s] = clock64();
                 commit_elect_a(f0 + 8 * s);
             }
+            if (TL && lane == 0 && blockIdx.x == 0)
+                printf("  mma warp: tempty wait %.1f per stage, arrive->seen %.1f\n", double(wt) / T, double(lat2) / (T - 2));
         }
     } else {
         const int e = warp - 1;
@@ -136,23 +177,36 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) epi_bench(int T, long long *c
         for (int it = 0; it < T; it++) {
             const int s = it & 1;
             const uint32_t ph = (it >> 1) & 1;
+            long long w0 = 0, w1 = 0;
             if (MODE == 1) {
-                mbar_wait_a(f0 + 8 * s, ph);
+                if (TL) w0 = clock64();
+                wait_bar<WAIT>(f0 + 8 * s, ph);
+                if (TL) {
+                    w1 = clock64();
+                    wt += w1 - w0;
+                    lat1 += w1 - ts_commit[s];
+                }
                 fence_after();
             }
             const uint32_t ta = tb + ((uint32_t)(32 * quarter) << 16) + s * N + slice * COLS;
-            const uint32_t o = drain<LD>(ta);
+            const uint32_t o = drain<LD>(ta, (MODE == 1 && ARR == 3) ? e0 + 8 * s : 0u);
             if (__any_sync(0xffffffffu, o & 0x80008000u)) acc += o;
             if (MODE == 1) {
                 fence_before();
                 if (ARR == 1) {
                     mbar_arrive_a(e0 + 8 * s);
+                } else if (ARR == 3) {
                 } else {
                     if (ARR == 0) __syncwarp();
+                    if (TL && e == E - 1 && lane == 0) ts_arrive[s] = clock64();
                     if (lane == 0) mbar_arrive_a(e0 + 8 * s);
                 }
+                if (TL) work += clock64() - w1;
             }
         }
+        if (TL && (e == 0 || e == E - 1) && lane == 0 && blockIdx.x == 0)
+            printf("  epi warp %d: tfull wait %.1f per stage, commit->seen %.1f, ld+or+arrive %.1f\n", e, double(wt) / T,
+                   double(lat1) / T, double(work) / T);
     }
     long long t1 = clock64();
     __syncthreads();
@@ -163,11 +217,63 @@ __global__ void __launch_bounds__(32 * (1 + E), 1) epi_bench(int T, long long *c
     if (warp == 0) tmem_dealloc(tb, 512);
 }
 
-template <int MODE, int KT, int E, int LD, int ARR>
+// MMA issue rate alone: one warp issues T MMAs of M = 128 x NN x K = 32 back to back (a commit
+// every 8), waits for the last; cycles per MMA
+template <int NN>
+__global__ void __launch_bounds__(32, 1) mma_only(int T, long long *cycles) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    tmem_alloc(&tbase, 512);
+    for (int i = threadIdx.x; i < (M + N) * 32; i += 32) sm[i] = (unsigned char)((i * 7 + 3) % 5 - 2);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    fence_async_smem();
+    fence_before();
+    __syncwarp();
+    fence_after();
+    const uint32_t tb = tbase;
+    const uint32_t id = idesc_i8(M, NN);
+    const uint64_t ad = sdesc(smem_u32(sm), M * 16, 128), bd = sdesc(smem_u32(sm + M * 32), N * 16, 128);
+    const long long t0 = clock64();
+    uint32_t ph = 0;
+    for (int it = 0; it < T; it += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) mma_i8_elect(tb + ((it / 8) & 1) * 256, ad, bd, id, k > 0);
+        commit_elect_a(smem_u32(&bar));
+        if ((it / 8) & 1) {  // every 16 MMAs: drain (keeps the issue queue bounded)
+            mbar_wait_a(smem_u32(&bar), ph);
+            ph ^= 1;
+            mbar_wait_a(smem_u32(&bar), ph);
+            ph ^= 1;
+        }
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+    fence_before();
+    __syncwarp();
+    tmem_dealloc(tb, 512);
+}
+template <int NN>
+void run_mma(int nsm, long long *dcyc) {
+    const int T = 16 * 2000;
+    CK(cudaFuncSetAttribute(mma_only<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int((M + N) * 32)));
+    mma_only<NN><<<nsm, 32, (M + N) * 32>>>(T, dcyc);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> cyc(nsm);
+    CK(cudaMemcpy(cyc.data(), dcyc, nsm * 8, cudaMemcpyDeviceToHost));
+    double avg = 0;
+    for (long long c : cyc) avg += double(c);
+    printf("mma only M=128 N=%3d K=32 i8: %6.1f cycles per MMA\n", NN, avg / nsm / T);
+}
+
+template <int MODE, int KT, int E, int LD, int ARR, int WAIT = 0, int TL = 0>
 void run(int T, int nsm, long long *dcyc, int *dout) {
     constexpr int KB = 32 * (KT > 0 ? KT : 1);
     const size_t smem = size_t(M + N) * KB;
-    auto kern = epi_bench<MODE, KT, E, LD, ARR>;
+    auto kern = epi_bench<MODE, KT, E, LD, ARR, WAIT, TL>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<nsm, 32 * (1 + E), smem>>>(16, dcyc, dout);
     CK(cudaDeviceSynchronize());
@@ -179,9 +285,10 @@ void run(int T, int nsm, long long *dcyc, int *dout) {
     for (long long c : cyc) avg += double(c);
     avg /= nsm;
     static const char *ldn[] = {"x64pack", "2x32pack", "2x32plain", "x32pack"};
-    static const char *arn[] = {"lane0+sync", "all-lane", "lane0"};
-    printf("mode=%d KT=%d E=%2d ld=%-9s arrive=%-10s: %7.1f cyc per stage (MMA floor %d)\n", MODE, KT, E, ldn[LD],
-           arn[ARR], avg / T, 128 * KT);
+    static const char *arn[] = {"lane0+sync", "all-lane", "lane0", "early"};
+    static const char *wn[] = {"try+hint", "try", "test"};
+    printf("mode=%d KT=%d E=%2d ld=%-9s arrive=%-10s wait=%-8s: %7.1f cyc per stage (MMA floor %d)\n", MODE, KT, E,
+           ldn[LD], arn[ARR], wn[WAIT], avg / T, 128 * KT);
 }
 
 int main(int argc, char **argv) {
@@ -194,6 +301,10 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&dcyc, nsm * 8));
     CK(cudaMalloc(&dout, nsm * 4));
     printf("device %s, %d SMs, T=%d stages per SM\n", prop.name, nsm, T);
+    run_mma<256>(nsm, dcyc);
+    run_mma<128>(nsm, dcyc);
+    run_mma<64>(nsm, dcyc);
+    run_mma<192>(nsm, dcyc);
     // TMEM read throughput alone
     run<0, 0, 8, 0, 0>(T, nsm, dcyc, dout);
     run<0, 0, 8, 1, 0>(T, nsm, dcyc, dout);
@@ -214,6 +325,20 @@ int main(int argc, char **argv) {
     run<1, 2, 8, 0, 1>(T, nsm, dcyc, dout);
     run<1, 2, 8, 0, 2>(T, nsm, dcyc, dout);
     run<1, 2, 16, 3, 2>(T, nsm, dcyc, dout);
+    // the wait flavour
+    run<1, 0, 8, 0, 2, 1>(T, nsm, dcyc, dout);
+    run<1, 0, 8, 0, 2, 2>(T, nsm, dcyc, dout);
+    run<1, 1, 8, 0, 2, 1>(T, nsm, dcyc, dout);
+    run<1, 1, 8, 0, 2, 2>(T, nsm, dcyc, dout);
+    run<1, 2, 8, 0, 2, 1>(T, nsm, dcyc, dout);
+    run<1, 2, 8, 0, 2, 2>(T, nsm, dcyc, dout);
+    run<1, 3, 8, 0, 2, 0>(T, nsm, dcyc, dout);
+    run<1, 3, 8, 0, 2, 2>(T, nsm, dcyc, dout);
+    // release right after the load
+    run<1, 0, 8, 0, 3>(T, nsm, dcyc, dout);
+    run<1, 1, 8, 0, 3>(T, nsm, dcyc, dout);
+    run<1, 2, 8, 0, 3>(T, nsm, dcyc, dout);
+    run<1, 3, 8, 0, 3>(T, nsm, dcyc, dout);
     printf("done\n");
     return 0;
 }
