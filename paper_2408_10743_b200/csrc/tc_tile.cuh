@@ -113,10 +113,39 @@ __device__ __forceinline__ void tc_gather(const uint32_t *sg, const short *mk, i
 __device__ __forceinline__ int tc_slot(int c) { return c % kTcSlots; }
 __device__ __forceinline__ uint32_t tc_slot_par(int c) { return (c / kTcSlots) & 1; }
 
+#ifdef SDB_TC_TRACE
+// Timeline of block 0 (variant builds): SM clock stamps per stage / head tile of the MMA warp
+// (actor 0), the epilogue warps (1..8) and one producer warp per group (9, 10); printed by the
+// last launch's block 0 at exit, analysed offline (tools/tc_trace.py).
+constexpr int kTrN = 192, kTrS0 = 3000, kTrC0 = 300;
+__device__ long long g_tct[12][4][kTrN];
+#define TCT(actor, ev, idx, base)                                                         \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && unsigned((idx) - (base)) < unsigned(kTrN) && (threadIdx.x & 31) == 0) \
+            g_tct[actor][ev][(idx) - (base)] = clock64();                                 \
+    } while (0)
+#define TCT_V(actor, ev, idx, base, val)                                                  \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && unsigned((idx) - (base)) < unsigned(kTrN) && (threadIdx.x & 31) == 0) \
+            g_tct[actor][ev][(idx) - (base)] = (val);                                     \
+    } while (0)
+#else
+#define TCT(actor, ev, idx, base)
+#define TCT_V(actor, ev, idx, base, val)
+#endif
 #ifdef SDB_TC_LAT
 // signalling latencies between the MMA warp and the epilogue (variant builds): SM clock stamps
 // through shared memory; block 0 prints the averages
 __device__ unsigned long long g_tc_lat[8];
+#endif
+// Unroll factor of the epilogue's stage loop. Inside an unrolled body ptxas hoists the next
+// stage's tfull wait into the current stage's OR tree; the best factor follows the tail tiles per
+// chunk, which follow the row bytes (measured on the g = 9 levels: K = 64, nbt = 10: 4.64 ms with
+// 4, 4.90 with 2, 4.85 with 1; K = 96, nbt = 5: 127.1 ms with 2, 132.2 with 1, 139.9 with 4).
+#ifdef SDB_TC_EPI_UNROLL
+template <int KW> constexpr int kTcEpiUnroll = SDB_TC_EPI_UNROLL;
+#else
+template <int KW> constexpr int kTcEpiUnroll = KW <= 2 ? 4 : 2;
 #endif
 struct TcShared {
 #ifdef SDB_TC_LAT
@@ -214,8 +243,10 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
         tc_gather<H, KW, false>(sg, mk, 0, 0, e, sw, cnt);
         const int c = c0 + a, s = tc_slot(c);
         SDB_CHECK(s >= 0 && s < kTcSlots && (H == 0 || e[H - 1] < d.b) && pt < kTcHeads);
+        if (pt < 32) TCT(9 + g, 0, c, kTrC0);
         if (lane == 0) tc::mbar_wait_a(bar_at(bars.aempty, s), tc_slot_par(c) ^ 1);
         __syncwarp();
+        if (pt < 32) TCT(9 + g, 1, c, kTrC0);
         unsigned char *tile = sA + size_t(s) * a_slot;
 #pragma unroll
         for (int w = 0; w < KW; w++)
@@ -237,6 +268,7 @@ __device__ int tc_write_heads(const TcUnitDesc &d, const TcGammaDev &gm, int g, 
         tc::fence_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_a(bar_at(bars.afull, s));
+        if (pt < 32) TCT(9 + g, 2, c, kTrC0);
         wrote++;
     }
     return wrote;
@@ -289,7 +321,7 @@ template <int KT>
 __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t b_tile16, int nbt, int bslot0,
                                               uint32_t bpar0, int nsb, bool bwait, bool release, uint32_t tbase,
                                               uint32_t idesc, uint32_t &st, uint32_t &tpar,
-                                              const TcBars &bars TCP_PARAMS TCG_PARAMS) {
+                                              const TcBars &bars TCP_PARAMS TCG_PARAMS, int &sidx, int ctile) {
     int slot = bslot0;
     uint32_t bpar = bpar0;
     for (int nb = 0; nb < nbt; nb++) {
@@ -327,8 +359,12 @@ __device__ __forceinline__ void tc_mma_stages(uint64_t aT, uint64_t bD, uint32_t
         if (release) tc::commit_elect_a(bar_at(bars.bempty, slot));
         TCP_END(4)
 #else
+        TCT(0, 0, sidx, kTrS0);
+        TCT_V(11, 0, sidx, kTrS0, ctile);
         tc::mma_stage<KT>(bar_at(bars.tempty, st), tpar ^ 1, bar_at(bars.bfull, slot), bpar, bwait, dT, aT, bT,
                           2 * kTcHeads, 2 * kTcTileN, idesc, bar_at(bars.tfull, st), bar_at(bars.bempty, slot), release);
+        TCT(0, 1, sidx, kTrS0);
+        sidx++;
 #ifdef SDB_TC_LAT
         if ((threadIdx.x & 31) == 0) {
             const long long now = clock64();
@@ -355,10 +391,11 @@ template <int KT>
 __device__ __forceinline__ void tc_mma_unit(int na, int nbt, bool restage, bool chunk_last, int &c, uint64_t aD,
                                             uint32_t a_slot16, uint64_t bD, uint32_t b_tile16, int bslot0,
                                             uint32_t bpar0, int nsb, uint32_t tbase, uint32_t idesc, uint32_t &st,
-                                            uint32_t &tpar, const TcBars &bars TCP_PARAMS TCGU_PARAMS) {
+                                            uint32_t &tpar, const TcBars &bars TCP_PARAMS TCGU_PARAMS, int &sidx) {
     for (int a = 0; a < na; a++, c++) {
         const int s = tc_slot(c);
         const uint64_t aT = aD + uint64_t(uint32_t(s) * a_slot16);
+        TCT(0, 2, sidx, kTrS0);
 #ifndef SDB_TC_MMA_NOAFULL
 #ifdef SDB_TC_GAPS
         const unsigned long long aw0 = clock64();
@@ -372,9 +409,51 @@ __device__ __forceinline__ void tc_mma_unit(int na, int nbt, bool restage, bool 
 #endif
         // the tail tiles were written for the chunk's first head tile; its last frees the slots
         tc_mma_stages<KT>(aT, bD, b_tile16, nbt, bslot0, bpar0, nsb, restage && a == 0, chunk_last && a == na - 1,
-                          tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1));
+                          tbase, idesc, st, tpar, bars TCP_ARGS TCG_ARGS(a == 0 ? 2 : 1), sidx, c);
         tc::commit_elect_a(bar_at(bars.aempty, s));
     }
+}
+
+#ifdef SDB_TC_COUNT_RARE
+__device__ unsigned long long g_tc_rare[4];  // calls, flagged rows, flagged (row, stage) pairs (variant builds)
+#endif
+// Rare path of the epilogue, once per head tile and out of line (its registers stay out of the
+// stage loop): some head row of the warp met a pair below the folded threshold in the stages of
+// `stage_hits`. The TMEM stages are long released, so the warp recomputes: for each flagged
+// (row, stage) its lanes take the stage's 128 columns of this warp's half through the exact
+// path (exact weight against the current bound, syndromes, key). Returns the warp's new bound.
+template <int W>
+__device__ __noinline__ unsigned tc_rare_rows(const ProblemDev p, const TilePlan tl, const uint32_t *s_rows,
+                                              const unsigned long long *s_binom, int BKs, const TileUnit *un,
+                                              unsigned stage_hits, int hoff, int half, int nbt, int ntails, int nheads,
+                                              unsigned thrH) {
+    const int lane = threadIdx.x & 31;
+    unsigned rows_hit = __ballot_sync(0xffffffffu, stage_hits != 0);
+#ifdef SDB_TC_COUNT_RARE
+    if (lane == 0) {
+        atomicAdd(&g_tc_rare[0], 1ull);
+        atomicAdd(&g_tc_rare[1], (unsigned long long)__popc(rows_hit));
+    }
+    atomicAdd(&g_tc_rare[2], (unsigned long long)__popc(stage_hits));
+#endif
+    while (rows_hit) {
+        const int L = __ffs(rows_hit) - 1;
+        rows_hit &= rows_hit - 1;
+        unsigned stL = __shfl_sync(0xffffffffu, stage_hits, L);
+        const int hoffL = __shfl_sync(0xffffffffu, hoff, L);
+        while (stL) {
+            const int nb = __ffs(stL) - 1;
+            stL &= stL - 1;
+#pragma unroll 1
+            for (int i = lane; i < 128; i += 32) {
+                const int y = nb * kTcTileN + half * 128 + i;  // B row of the unit
+                const int tix = min((y % (kTcProdWarps * 32)) * nbt + y / (kTcProdWarps * 32), ntails - 1);
+                SDB_CHECK(tix >= 0 && tix < ntails && hoffL >= 0 && hoffL < nheads);
+                thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, un, hoffL, tix, thrH);
+            }
+        }
+    }
+    return __reduce_min_sync(0xffffffffu, thrH);  // the bound is global
 }
 
 template <int W, int KW>
@@ -461,6 +540,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
             TcGaps gaps;
 #endif
             int c = 0;
+            int sidx = 0;
             TCP_DECL
             const unsigned long long tcp_start = clock64();
             for (int u = 0;; u++) {
@@ -500,11 +580,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #define SDB_TC_UNIT(k)                                                                                       \
     case k:                                                                                                  \
         tc_mma_unit<k>(na, nbt, restage, chunk_last, c, aD, a_slot16, bD, b_tile16, bslot_c, bpar_c, nsb, tb_u, \
-                       idesc, st, tpar, bars TCP_ARGS TCGU_ARGS);                                            \
+                       idesc, st, tpar, bars TCP_ARGS TCGU_ARGS, sidx);                                      \
         break;
                     SDB_TC_UNIT(1) SDB_TC_UNIT(2) SDB_TC_UNIT(3)
                     default: tc_mma_unit<4>(na, nbt, restage, chunk_last, c, aD, a_slot16, bD, b_tile16, bslot_c, bpar_c,
-                                            nsb, tb_u, idesc, st, tpar, bars TCP_ARGS TCGU_ARGS);
+                                            nsb, tb_u, idesc, st, tpar, bars TCP_ARGS TCGU_ARGS, sidx);
                         break;
 #undef SDB_TC_UNIT
                 }
@@ -527,6 +607,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
         const uint32_t tf_x = tf_st ^ bar_at(bars.tfull, 1), te_x = te_st ^ bar_at(bars.tempty, 1),
                        ta_x = ta0 ^ (ta0 + uint32_t(kTcTileN));
         int c = 0;  // head tiles consumed
+        int sidx = 0;
 #ifdef SDB_TC_LAT
         long long lat_r[4] = {0, 0, 0, 0};
 #endif
@@ -564,12 +645,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 // behind that tile's stages) tightens the bound now; load the next one
                 thrH = min(thrH, wmin_next);
                 wmin_next = ld_relaxed_u32(&p.state->wmin);
+                unsigned stage_hits = 0;  // bit nb: this row has a pair below the folded threshold in stage nb
+#pragma unroll kTcEpiUnroll<KW>
                 for (int nb = 0; nb < d.nbt; nb++) {
                     TCP_BEGIN
 #ifdef SDB_TC_LAT
                     const long long lat_enter = clock64();
 #endif
+                    TCT(warp, 0, sidx, kTrS0);
                     tc::mbar_wait_a(tf_st, tpar_e);
+                    TCT(warp, 1, sidx, kTrS0);
                     TCP_END(2)
 #ifdef SDB_TC_LAT
                     const long long lat_seen = clock64();
@@ -594,11 +679,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                     // critical path, the sign test is not)
                     tc::fence_before();
                     tc::mbar_arrive_a(te_st);
+                    TCT(warp, 2, sidx, kTrS0);
                     // a pair passes the folded threshold iff its 16-bit accumulator is negative:
                     // OR the packed words as a tree of 3-input ORs (depth 4; ptxas turns a plain OR
-                    // reduction into one 32-deep dependent LOP3 chain), test the two sign bits.
-                    // The second level (8 groups of 18 columns; the last holds 2) is kept to
-                    // locate a hit.
+                    // reduction into one 32-deep dependent LOP3 chain) and note, per head row, the
+                    // stages whose two sign bits come out set. No vote and no branch here: the
+                    // rows are looked at once per head tile.
                     uint32_t r[22];
 #pragma unroll
                     for (int i = 0; i < 21; i++) r[i] = tc::or3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
@@ -611,42 +697,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
 #if defined(SDB_TC_NOMMA) || defined(SDB_TC_NOPROD)
                     o = 0;  // TMEM / the operands hold no real data
 #endif
-                    if (__any_sync(0xffffffffu, o & 0x80008000u)) {
-                        // rare: some head row of this warp has a pair below the folded threshold
-                        // in one of its column groups. The stage is already released, so the
-                        // warp recomputes: for each flagged row, its lanes take the columns of the
-                        // flagged groups through the exact path (exact weight against the
-                        // current bound, syndromes, key) — 18 candidates per flagged group.
-                        unsigned gmask = 0;
-#pragma unroll
-                        for (int i = 0; i < 8; i++) gmask |= (r2[i] & 0x80008000u) ? 1u << i : 0u;
-                        if (hoff >= d.nheads) gmask = 0;  // rows past the unit's heads never pass
-                        unsigned rows_hit = __ballot_sync(0xffffffffu, gmask != 0);
-                        while (rows_hit) {
-                            const int L = __ffs(rows_hit) - 1;
-                            rows_hit &= rows_hit - 1;
-                            const unsigned gmL = __shfl_sync(0xffffffffu, gmask, L);
-                            const int hoffL = __shfl_sync(0xffffffffu, hoff, L);
-#pragma unroll 1
-                            for (int i = lane; i < 128; i += 32) {
-                                if (!((gmL >> (i / 18)) & 1u)) continue;
-                                const int y = nb * kTcTileN + half * 128 + i;  // B row of the unit
-                                const int tix = min((y % (kTcProdWarps * 32)) * d.nbt + y / (kTcProdWarps * 32),
-                                                    d.ntails - 1);
-                                SDB_CHECK(tix >= 0 && tix < d.ntails && hoffL >= 0 && hoffL < d.nheads);
-                                thrH = tile_exact<W>(p, tl, s_rows, s_binom, BKs, &un, hoffL, tix, thrH);
-                            }
-                        }
-                        thrH = __reduce_min_sync(0xffffffffu, thrH);  // the bound is global
-                    }
+                    if (o & 0x80008000u) stage_hits |= 1u << nb;
                     // next stage: flip the TMEM stage (and the phase parity after stage 1)
                     tf_st ^= tf_x;
                     te_st ^= te_x;
                     ta_st ^= ta_x;
                     tpar_e ^= st_e;
                     st_e ^= 1u;
+                    TCT(warp, 3, sidx, kTrS0);
+                    sidx++;
                     TCP_END(3)
                 }
+                if (hoff >= d.nheads) stage_hits = 0;  // rows past the unit's heads never pass
+                if (__any_sync(0xffffffffu, stage_hits != 0))
+                    thrH = tc_rare_rows<W>(p, tl, s_rows, s_binom, BKs, &un, stage_hits, hoff, half, d.nbt, d.ntails,
+                                           d.nheads, thrH);
                 // hand a tighter bound to the producers' next head tiles (s_thr_seen is
                 // warp-uniform; the loop above is too, so the whole warp gets here)
                 if (__any_sync(0xffffffffu, thrH < s_thr_seen)) {
@@ -806,6 +871,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc(tbase, 512);
+#ifdef SDB_TC_COUNT_RARE
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("[tcrare] cumulative: calls %llu rows %llu (row, stage) pairs %llu\n", g_tc_rare[0], g_tc_rare[1], g_tc_rare[2]);
+#endif
+#ifdef SDB_TC_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_tct[0][0][kTrN - 1] != 0) {
+        const long long t0 = g_tct[0][0][0];
+        for (int a = 0; a < 12; a++)
+            for (int e = 0; e < 4; e++)
+                for (int i = 0; i < kTrN; i += 8) {
+                    const long long *v = &g_tct[a][e][i];
+                    const long long b = a == 11 ? 0 : t0;
+                    printf("[tct] %d %d %d %lld %lld %lld %lld %lld %lld %lld %lld\n", a, e, i, v[0] ? v[0] - b : -1,
+                           v[1] ? v[1] - b : -1, v[2] ? v[2] - b : -1, v[3] ? v[3] - b : -1, v[4] ? v[4] - b : -1,
+                           v[5] ? v[5] - b : -1, v[6] ? v[6] - b : -1, v[7] ? v[7] - b : -1);
+                }
+        for (int a = 0; a < 12; a++)
+            for (int e = 0; e < 4; e++)
+                for (int i = 0; i < kTrN; i++) g_tct[a][e][i] = 0;
+    }
+#endif
     if (threadIdx.x == 0 && s_visited) atomicAdd(&p.state->visited, s_visited);
 }
 
