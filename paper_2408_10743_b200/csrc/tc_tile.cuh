@@ -140,12 +140,13 @@ __device__ unsigned long long g_tc_lat[8];
 #endif
 // Unroll factor of the epilogue's stage loop. Inside an unrolled body ptxas hoists the next
 // stage's tfull wait into the current stage's OR tree; the best factor follows the tail tiles per
-// chunk, which follow the row bytes (measured on the g = 9 levels: K = 64, nbt = 10: 4.64 ms with
-// 4, 4.90 with 2, 4.85 with 1; K = 96, nbt = 5: 127.1 ms with 2, 132.2 with 1, 139.9 with 4).
+// chunk, which follow the row bytes (measured on the g = 9 levels: K = 64, nbt = 10: 4.51 ms with
+// 5, 4.64 with 3 or 4, 4.73 with 8, 4.90 with 2, 4.85 with 1; K = 96, nbt = 5: 126.8 ms with 2 or 3, 129.9 with 5,
+// 132.2 with 1, 139.9 with 4).
 #ifdef SDB_TC_EPI_UNROLL
 template <int KW> constexpr int kTcEpiUnroll = SDB_TC_EPI_UNROLL;
 #else
-template <int KW> constexpr int kTcEpiUnroll = KW <= 2 ? 4 : 2;
+template <int KW> constexpr int kTcEpiUnroll = KW <= 2 ? 5 : 2;
 #endif
 struct TcShared {
 #ifdef SDB_TC_LAT

@@ -50,3 +50,29 @@ if len(sys.argv) > 2:
     for i in range(int(sys.argv[2]), int(sys.argv[2]) + 12):
         print(i, "tile", tile[i], "mma", m0[i] - m1[4], m1[i] - m1[4], "| epi seen/release:",
               " ".join(f"{E[w][1][i]-m1[4]}/{E[w][2][i]-m1[4]}" for w in range(1, 9)))
+# head-tile starts: previous stage's commit issue -> tile begin -> after the afull wait -> commit issue,
+# and the epilogue's iteration end -> next wait enter at the same boundary
+print("tile starts: prev commit -> tile begin | afull wait | stage block (tempty wait + issue) | epilogue warp 1/4 boundary gap")
+for i in starts[:12]:
+    print(i, mt[i] - m1[i - 1], "|", m0[i] - mt[i], "|", m1[i] - m0[i], "|", E[1][0][i] - E[1][3][i - 1], E[4][0][i] - E[4][3][i - 1],
+          "| seen-commit w1/w4:", E[1][1][i] - m1[i], E[4][1][i] - m1[i])
+ins = [i for i in ok if i not in starts][:6]
+print("in-tile for comparison: stage block | epilogue gap w1/w4")
+for i in ins:
+    print(i, m1[i] - m0[i], "|", E[1][0][i] - E[1][3][i - 1], E[4][0][i] - E[4][3][i - 1])
+# producers (one warp per group: actors 9, 10), by head tile: enter the aempty wait, slot free, tile
+# published, against the MMA warp's arrival at the tile
+P = {g: [rows.get((9 + g, e), {}) for e in range(3)] for g in range(2)}
+c0 = 300  # kTrC0
+print("tile: producer enter / slot free / published | MMA reaches the tile | afull seen  (cycles, same origin)")
+base = m1[4]
+for i in starts[:14]:
+    c = tile[i]
+    g = None
+    for gg in range(2):
+        if (c - c0) in P[gg][0] and P[gg][0][c - c0] > 0:
+            g = gg
+    if g is None:
+        continue
+    pe, pf, pp = (P[g][e].get(c - c0, -1) for e in range(3))
+    print(c, "group", g, pe - base, pf - base, pp - base, "|", mt[i] - base, "|", m0[i] - base, "| published - reached:", pp - mt[i])
