@@ -3,23 +3,31 @@
 // POPC tile kernel.
 //
 // Warp roles, one CTA per SM (kTcThreads = 576):
-//   warp 0        TMEM owner (512 columns: two 128 x 256 s32 stages); lane 0 issues the MMAs
-//   warps 1..8    epilogue: tcgen05.ld pack::16b -> packed 16-bit minimum -> threshold test
-//   warp 9        unit warp: claims units and publishes their descriptors
+//   warp 0        TMEM owner (512 columns: two 128 x 256 s32 stages) and MMA issuer: a converged
+//                 warp, one PTX block per stage (tc::mma_stage: wait, elected MMAs, commits)
+//   warps 1..8    epilogue: one tcgen05.ld x64 pack::16b per stage, the stage handed back right
+//                 after the load, an OR tree over the packed words, a per-row bitmask of the
+//                 stages whose sign bits came out set; once per head tile a vote, and for the
+//                 flagged (row, stage) pairs the exact path on recomputed pairs (tc_rare_rows)
+//   warp 9        unit warp: claims units and publishes their descriptors, one unit ahead
 //   warps 10..17  producers, two groups of four: group g writes the head tiles c with
 //                 c % 2 == g (A, a ring of four; thread r of the group writes row r), and all
-//                 256 threads write the unit's tails (B, two buffers) when its chunk changes —
+//                 256 threads write the chunk's tail tiles (B, a ring of nbt + 1 slots) —
 //                 int8 coordinates in the canonical K-major no-swizzle layout (8-row x 16-byte
 //                 core matrices)
-// Pipelines (mbarriers): unit queue full/empty, A slot full/empty, B buffer full/empty, TMEM
+// Pipelines (mbarriers): unit queue full/empty, A slot full/empty, B slot full/empty, TMEM
 // stage full/empty. No CTA-wide barrier after the start: every warp signals its own part, so
 // warps drift freely within the rings.
 //
-// A unit is (Gamma j, boundary b, up to 1024 heads, up to 256 nbt tails): its na <= 8 head
-// tiles each meet all of its nbt tail tiles. Head row r of the unit's tiles walks na
+// A unit is (Gamma j, boundary b, up to 128 * kTcUnitTiles heads, up to 256 nbt tails): its na
+// head tiles each meet all of its nbt tail tiles. Head row r of the unit's tiles walks na
 // consecutive colex ranks (successor steps); a producer thread's nbt tails are consecutive
 // ranks too. Element lists stay in registers: the producer routines are compiled per element
 // count (h, t - 1 <= kTcMaxPart) and per sign words per row (KW).
+//
+// Variant builds (tools/build_variant.sh): SDB_TC_TRACE (clock-stamped timeline of block 0,
+// tools/tc_trace.py), SDB_TC_LAT (signalling latencies), SDB_TC_GAPS / SDB_TC_PROF (MMA-warp
+// gaps and waits), SDB_TC_NOPROD / SDB_TC_NOMMA (pipeline bisection), SDB_TC_COUNT_RARE.
 #pragma once
 
 #include "tc_ptx.cuh"
@@ -147,6 +155,9 @@ __device__ unsigned long long g_tc_lat[8];
 template <int KW> constexpr int kTcEpiUnroll = SDB_TC_EPI_UNROLL;
 #else
 template <int KW> constexpr int kTcEpiUnroll = KW <= 2 ? 5 : 2;
+#endif
+#ifndef SDB_TC_RUN
+#define SDB_TC_RUN 8  // units claimed per dispenser atomic (measured g = 9: 4.51 / 4.48 / 4.53 ms with 4 / 8 / 16)
 #endif
 struct TcShared {
 #ifdef SDB_TC_LAT
@@ -736,7 +747,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_tile_kernel(ProblemDev p, Tc
                 for (;;) {
                     d = TcUnitDesc{};
                     if (claim == claim_end) {
-                        const unsigned long long run = seen + 4ull * 4 * gridDim.x < local_units ? 4ull : 1ull;
+                        // consecutive units mostly share their tail chunk: longer runs restage less
+                        // often; single units near the end keep the SMs level
+                        constexpr unsigned long long kRun = SDB_TC_RUN;
+                        const unsigned long long run = seen + kRun * 4 * gridDim.x < local_units ? kRun : 1ull;
                         claim = atomicAdd(tl.counter, run);
                         claim_end = claim + run;
                         seen = claim_end;
